@@ -1,0 +1,351 @@
+"""Benchmark: MG-PCG solve of the SIMP elasticity system on one B200 per rank.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl b200|reference]
+
+A step is one drop-in call of the hot path on the config's workload: element
+moduli from rho, K(rho), hierarchy build, PCG to rtol=1e-8, compliance and
+sensitivity -- what one topology-optimisation iteration costs (the reference
+rebuilds the preconditioner every iteration, optimization.py:498 design note).
+Metric: DOF*iterations/s (higher is better) = sum(ndof*iters) / sum(step time).
+Inputs are resident in HBM when the timed region starts; L2 is flushed before
+every timed step.  ``e2e`` repeats the metric through the C-ABI host-buffer entry
+point (tmg_solve_compliance_host) with H2D/D2H copies inside the timed region.
+``--impl reference`` times the CPU oracle port of the reference algorithm on a
+bounded sample (setup + a fixed number of PCG iterations) on rank 0.
+Under torchrun every rank runs an independent replica (scaling: weak).
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MG-PCG DOF*iterations/s (setup+solve+sensitivity per step)"
+UNIT = "DOF*iter/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--cpu-sample-iters", type=int, default=10)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def gmg_legs(w):
+    return [s for s in w.solvers if s["strategy"] == "gmg"]
+
+
+def config_dict(w, args, world, legs, pending):
+    return {"workload": w.name, "config_index": args.config, "ndof": int(w.ndof),
+            "elements": int(w.mesh.element_count), "legs": legs, "pending_legs": pending,
+            "rtol": w.rtol, "precision": "fp64", "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": "replicas x%d" % world}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.err = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable: %s" % self.err]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(w, leg, iters):
+    from oracle import topomg_oracle as O
+    from paper_2001_01655_b200 import problems
+    g = O.make_grid(w.mesh.dims)
+    t0 = time.perf_counter()
+    E = O.simp_modulus(w.rho, problems.PENAL, problems.E0, problems.EMIN)
+    K = O.assemble_stiffness(g, w.bc.fixed_dofs, E)
+    if leg["smoother"] == "chebyshev":
+        sm = O.Smoother("chebyshev", 1.0, leg.get("degree", 2))
+    else:
+        sm = O.Smoother(leg["smoother"], leg.get("weight", 0.5))
+    h = O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+    u, rec = O.pcg(K, w.bc.load_vector, None, h.apply, rtol=w.rtol, max_iterations=iters)
+    O.compliance_sensitivity(g, w.bc.load_vector, u, w.rho, problems.PENAL, problems.E0, problems.EMIN)
+    dt = time.perf_counter() - t0
+    return w.ndof * rec.iterations, dt, rec.iterations
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2001_01655_b200 import problems
+    w = problems.CONFIGS[args.config]()
+    legs = gmg_legs(w)
+    work = secs = 0.0
+    for step in range(args.warmup + args.steps):
+        wk = dt = 0.0
+        for leg in legs:
+            a, b, _ = oracle_sample(w, leg, args.cpu_sample_iters)
+            wk += a
+            dt += b
+        if step >= args.warmup:
+            work += wk
+            secs += dt
+    value = work / secs
+    sample = "oracle port: setup + %d PCG iterations per leg (%s) per step" % (
+        args.cpu_sample_iters, ",".join("gmg%d" % l["levels"] for l in legs))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
+            "config": config_dict(w, args, 1, ["gmg%d" % l["levels"] for l in legs], []),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args, rank, world, local):
+    import torch
+
+    import paper_2001_01655_b200 as T
+    from paper_2001_01655_b200 import _lib, problems
+    from paper_2001_01655_b200._dev import as_dev, empty_dev, ptr, stream_ptr
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = problems.CONFIGS[args.config]()
+    legs = gmg_legs(w)
+    pending = [s["strategy"] for s in w.solvers if s["strategy"] != "gmg"]
+    L = _lib.load()
+    law = T.SimpLaw(penalty=problems.PENAL, e_min_ratio=problems.EMIN)
+    rho_d = as_dev(w.rho)
+    f_d = as_dev(w.bc.load_vector)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    state = {}
+
+    def step():
+        work = 0
+        iters = []
+        for leg in legs:
+            E = law.modulus(rho_d)
+            K = T.StiffnessOperator(w.mesh, w.bc, E)
+            sm = problems.gmg_settings(leg)
+            h = T.build_gmg(w.mesh, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+            u, rec = T.cg_solve(K, f_d, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=20000))
+            dc = empty_dev(w.mesh.element_count)
+            comp = C.c_double()
+            _lib.check(L.tmg_compliance_sensitivity(K.handle, ptr(rho_d), ptr(f_d), ptr(u), law.penalty,
+                                                    law.e_max, law.e_min, ptr(dc), C.byref(comp),
+                                                    stream_ptr(None)))
+            work += w.ndof * rec.iterations
+            iters.append(rec.iterations)
+            state["K"], state["h"], state["rec"], state["compliance"] = K, h, rec, comp.value
+        return work, iters
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = L.tmg_launch_count()
+    total_ms, total_work, it_log = 0.0, 0, []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            wk, its = step()
+            e1.record()
+            torch.cuda.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            total_work += wk
+            it_log.append(its)
+    launches = L.tmg_launch_count() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * total_work / (total_ms / 1e3)
+
+    # dominant kernel: level-0 Jacobi sweep, timed live with CUDA events
+    roof = roofline(args, w, state, L)
+
+    # end to end through the C-ABI host entry point
+    e2e = e2e_run(args, w, legs, L, law)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
+            "config": config_dict(w, args, world, ["gmg%d" % l["levels"] for l in legs], pending),
+            "pcg_iterations": it_log[-1], "compliance": state["compliance"],
+            "solve_ms_last": state["rec"].solve_time * 1e3,
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        wk, dt, its = oracle_sample(w, legs[0], args.cpu_sample_iters)
+        line["cpu_baseline"] = {"value": wk / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": "oracle port (numpy/scipy, 1 thread): setup + %d PCG iterations "
+                                          "of the gmg%d leg, %.1f s" % (its, legs[0]["levels"], dt)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def roofline(args, w, state, L):
+    import torch
+
+    from paper_2001_01655_b200._dev import ptr
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    h = state["h"]
+    ms = C.c_double()
+    reps = 50
+    _lib_check = __import__("paper_2001_01655_b200._lib", fromlist=["check"]).check
+    _lib_check(L.tmg_hierarchy_time_smoother(h.handle, 0, reps, C.byref(ms),
+                                             torch.cuda.current_stream().cuda_stream))
+    mesh = w.mesh
+    d = mesh.ndim
+    nodes, nel = mesh.node_count, mesh.element_count
+    bytes_launch = nodes * (4 * 8 * d + 1) + nel * 8
+    achieved = bytes_launch / (ms.value / 1e3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get("config%d" % args.config, {}).get("jacobi_dram_bytes")
+    except Exception:  # noqa: BLE001
+        pass
+    return {"kernel": "k_jacobi<%d,FineOp> (level-0 weighted-Jacobi sweep, matrix-free K)" % d,
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "bytes_per_launch": bytes_launch, "launch_us": ms.value * 1e3,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+            "note": "working set %.1f MB (< 126 MB L2): the sweep can be L2-resident inside the solve"
+                    % (bytes_launch / 1e6)}
+
+
+def e2e_run(args, w, legs, L, law):
+    from paper_2001_01655_b200 import _lib
+    leg = legs[0]
+    sm = leg_desc(leg)
+    mg = _lib.MgDesc()
+    mg.strategy = 0
+    mg.coarse_max_dofs = 1
+    mg.max_levels = leg["levels"]
+    mg.smoother = sm
+    mg.n_pre, mg.n_post = leg["n_pre"], leg["n_post"]
+    cfg = _lib.SolveDesc(w.rtol, 20000)
+    rho = np.ascontiguousarray(w.rho, dtype=np.float64)
+    f = np.ascontiguousarray(w.bc.load_vector)
+    fixed = np.ascontiguousarray(w.bc.fixed_dofs, dtype=np.int64)
+    u = np.empty(w.ndof)
+    dc = np.empty(w.mesh.element_count)
+    comp = C.c_double()
+    rec = _lib.SolveRec()
+    md = _lib.mesh_desc(w.mesh)
+
+    def call():
+        _lib.check(L.tmg_solve_compliance_host(C.byref(md), rho.ctypes.data, fixed.ctypes.data, fixed.size,
+                                               f.ctypes.data, law.penalty, law.e_max, law.e_min, 0.3,
+                                               C.byref(mg), C.byref(cfg), u.ctypes.data, dc.ctypes.data,
+                                               C.byref(comp), C.byref(rec)))
+    call()
+    work = secs = 0.0
+    for _ in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        call()
+        secs += time.perf_counter() - t0
+        work += w.ndof * rec.iterations
+    h2d = rho.nbytes + f.nbytes + w.mesh.node_count + 8 * (24 * 24)
+    d2h = u.nbytes + dc.nbytes + 8 + 8
+    return {"value": work / secs, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "leg": "gmg%d" % leg["levels"], "ms_per_step": 1e3 * secs / max(1, args.e2e_steps),
+            "timing": "host wall clock around tmg_solve_compliance_host (host buffers in/out)"}
+
+
+def leg_desc(leg):
+    from paper_2001_01655_b200 import problems
+    return problems.gmg_settings(leg).desc()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * topomg_b200.h -- C ABI of the B200-native MG-PCG hot path.
+ *
+ * Drop-in boundary for the reference's solver/preconditioner interface
+ * (reference package `topomg`, /root/reference/pkg/src/topomg).  The reference
+ * is Python, so the binding a maintainer adds is a ctypes stub;
+ * paper_2001_01655_b200/_lib.py is exactly that stub.  Each entry point names
+ * the reference function it replaces.
+ *
+ * Conventions
+ *   - All vector arguments named *_dev are DEVICE pointers (fp64, DOF-interleaved:
+ *     dof = node*dofs_per_node + component, nodes lexicographic with x fastest,
+ *     exactly the reference numbering, mesh.py:15-111).
+ *   - Arguments named *_host are host pointers.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Every function returns 0 on success and a negative code on failure;
+ *     tmg_last_error() then holds a message (thread-local).  Invalid arguments
+ *     that the reference rejects with ValueError return TMG_EINVAL; an index
+ *     out of range (the reference's IndexError) returns TMG_ERANGE.
+ *   - There is no CPU fallback: without a CUDA device every compute entry point
+ *     returns TMG_ENODEV.
+ */
+#ifndef TOPOMG_B200_H
+#define TOPOMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMG_OK 0
+#define TMG_EINVAL (-1)  /* reference raises ValueError            */
+#define TMG_ERANGE (-2)  /* reference raises IndexError            */
+#define TMG_ECUDA (-3)   /* CUDA runtime failure                    */
+#define TMG_ENODEV (-4)  /* no CUDA device: the product never falls back to the CPU */
+#define TMG_ESTATE (-5)  /* solver failure (e.g. non-SPD coarse operator) */
+
+typedef struct tmg_operator tmg_operator;   /* K(rho) on a structured grid   */
+typedef struct tmg_hierarchy tmg_hierarchy; /* MgHierarchy                    */
+
+/* StructuredMesh (mesh.py:15): element counts per axis + element edge lengths. */
+typedef struct {
+  int32_t ndim;      /* 2 (Q4, plane stress) or 3 (Hex8) */
+  int32_t dims[3];   /* elements per axis (dims[2] ignored in 2D) */
+  double h[3];       /* element edge lengths */
+} tmg_mesh_desc;
+
+/* SmootherConfig (multigrid.py:30).  kind: 0 weighted_jacobi, 1 block_jacobi,
+ * 2 chebyshev (Jacobi-preconditioned Chebyshev of degree inner_iterations with a
+ * lanczos_steps-step Lanczos bound; extension required by BASELINE.json). */
+typedef struct {
+  int32_t kind;
+  double weight;
+  int32_t inner_iterations;
+  int32_t lanczos_steps;
+  uint64_t seed;
+} tmg_smoother_desc;
+
+/* SolveConfig (krylov.py:17) for the preconditioned CG extension. */
+typedef struct {
+  double rtol;            /* ||r|| <= rtol * ||b||, as krylov.py:63 */
+  int32_t max_iterations;
+} tmg_solve_desc;
+
+/* SolveRecord (krylov.py:31). */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double initial_residual;
+  double final_residual;  /* recursive residual at exit */
+  double solve_ms;        /* device time of the solve (CUDA events) */
+} tmg_solve_record;
+
+/* hierarchy level description (MgHierarchy.summary, multigrid.py:247) */
+typedef struct {
+  int64_t size;        /* rows of the level operator */
+  int64_t nonzeros;    /* stored scalar entries */
+  int32_t provenance;  /* 0 geometric, 1 algebraic */
+  int32_t storage;     /* 0 matrix-free element, 1 structured stencil, 2 BSR, 3 dense inverse */
+} tmg_level_info;
+
+const char* tmg_last_error(void);
+int tmg_version(void);
+int tmg_device_count(void);
+/* Number of this library's kernel launches so far (CUDA-graph replays included). */
+int64_t tmg_launch_count(void);
+
+/* mesh.py:254 element_stiffness -> row-major (4|8)*ndim square matrix. Host only. */
+int tmg_element_stiffness(const tmg_mesh_desc* mesh, double E, double nu, double* ke_host);
+
+/* material.py:175 SimpLaw.modulus on the device: E = emin + (e0-emin)*rho^p. */
+int tmg_simp_modulus(const double* rho_dev, int64_t n, double penalty, double e0, double emin,
+                     double* E_dev, void* stream);
+
+/* mesh.py:327 assemble_stiffness(mesh, bc, element_moduli): the operator is kept
+ * matrix-free (element moduli + KE); fixed dofs are eliminated symmetrically with a
+ * unit diagonal exactly as mesh.py:313.  fixed_dofs_host may contain duplicates.
+ * The moduli are copied; the caller's buffer may be freed afterwards. */
+int tmg_operator_create(const tmg_mesh_desc* mesh, const double* element_moduli_dev,
+                        const int64_t* fixed_dofs_host, int64_t n_fixed, double nu,
+                        void* stream, tmg_operator** out);
+int tmg_operator_destroy(tmg_operator* op);
+int64_t tmg_operator_size(const tmg_operator* op);
+/* y = K x  (K @ x in the reference) */
+int tmg_operator_apply(tmg_operator* op, const double* x_dev, double* y_dev, void* stream);
+/* K.diagonal() */
+int tmg_operator_diagonal(tmg_operator* op, double* d_dev, void* stream);
+
+/* multigrid.py:318 build_gmg(mesh, K, coarse_max_dofs, smoother, n_pre, n_post).
+ * max_levels <= 0 means no cap (reference behaviour). */
+int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels,
+                  const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
+                  void* stream, tmg_hierarchy** out);
+int tmg_hierarchy_destroy(tmg_hierarchy* h);
+int tmg_hierarchy_num_levels(const tmg_hierarchy* h);
+int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_info* info);
+/* multigrid.py:231 MgHierarchy.vcycle(b, k) (zero initial guess). */
+int tmg_hierarchy_vcycle(tmg_hierarchy* h, int32_t level, const double* b_dev, double* x_dev,
+                         void* stream);
+/* y = A^level x (the Galerkin operator of a level), for parity checks. */
+int tmg_hierarchy_level_apply(tmg_hierarchy* h, int32_t level, const double* x_dev,
+                              double* y_dev, void* stream);
+/* Chebyshev eigenvalue estimate of a level (NaN unless the smoother is chebyshev). */
+int tmg_hierarchy_level_lmax(tmg_hierarchy* h, int32_t level, double* lmax_host, void* stream);
+
+/* Average device time (ms, CUDA events on `stream`) of one smoother sweep kernel of
+ * a level (weighted/block Jacobi sweep or one Chebyshev step), over `reps` launches.
+ * Used by bench.py for the roofline of the dominant kernel. */
+int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, double* ms_host,
+                                void* stream);
+
+/* Preconditioned CG (extension; krylov.py:134 is the reference's GMRES entry).
+ * h may be NULL (unpreconditioned).  x_dev holds x0 on entry when use_x0 != 0
+ * and the solution on return.  residual_history_host (may be NULL) receives
+ * iterations+1 norms. Synchronises the stream once at the end. */
+int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b_dev, double* x_dev,
+                  int32_t use_x0, const tmg_solve_desc* cfg, double* residual_history_host,
+                  tmg_solve_record* rec, void* stream);
+
+/* optimization.py:106 element_strain_energies: ce_e = u_e^T KE u_e (unit modulus). */
+int tmg_strain_energy(tmg_operator* K, const double* u_dev, double* ce_dev, void* stream);
+/* optimization.py:128-129: dc_e = -p (e0-emin) rho_e^(p-1) ce_e, compliance = f.u */
+int tmg_compliance_sensitivity(tmg_operator* K, const double* rho_dev, const double* f_dev,
+                               const double* u_dev, double penalty, double e0, double emin,
+                               double* dc_dev, double* compliance_host, void* stream);
+
+/* End-to-end drop-in for compliance_and_sensitivity (optimization.py:114) given the
+ * filtered densities: HOST buffers in and out; H2D copies, modulus, operator,
+ * hierarchy (GMG: strategy 0), PCG solve, sensitivity and D2H copies all inside. */
+typedef struct {
+  int32_t strategy;          /* 0 gmg */
+  int64_t coarse_max_dofs;
+  int32_t max_levels;
+  tmg_smoother_desc smoother;
+  int32_t n_pre, n_post;
+} tmg_mg_desc;
+int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
+                              const int64_t* fixed_dofs_host, int64_t n_fixed,
+                              const double* f_host, double penalty, double e0, double emin,
+                              double nu, const tmg_mg_desc* mg, const tmg_solve_desc* cfg,
+                              double* u_host, double* dc_host, double* compliance_host,
+                              tmg_solve_record* rec);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPOMG_B200_H */

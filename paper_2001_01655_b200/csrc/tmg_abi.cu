@@ -1,0 +1,464 @@
+// C ABI (include/topomg_b200.h) over the B200 MG-PCG kernels.
+#include <cstring>
+#include <string>
+
+#include "../../include/topomg_b200.h"
+#include "tmg_pcg.cuh"
+
+using namespace tmg;
+
+struct tmg_operator {
+  Operator op;
+  std::unique_ptr<PcgCtx> pcg;  // unpreconditioned CG workspace
+};
+struct tmg_hierarchy {
+  std::unique_ptr<Hierarchy> h;
+  const tmg_operator* K = nullptr;
+  std::unique_ptr<PcgCtx> pcg;
+};
+
+static thread_local std::string g_err;
+
+#define ABI_BEGIN try {
+#define ABI_END                                   \
+  }                                               \
+  catch (const tmg::Error& e) {                   \
+    g_err = e.what();                             \
+    return e.code;                                \
+  }                                               \
+  catch (const std::exception& e) {               \
+    g_err = e.what();                             \
+    return TMG_ECUDA;                             \
+  }                                               \
+  return TMG_OK;
+
+static cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+static void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error(TMG_ENODEV, "no CUDA device: the B200 path has no CPU fallback");
+  }
+}
+
+static void check_mesh(const tmg_mesh_desc* m) {
+  TMG_REQUIRE(m != nullptr, "mesh descriptor is NULL");
+  TMG_REQUIRE(m->ndim == 2 || m->ndim == 3, "mesh must be 2D or 3D");
+  for (int d = 0; d < m->ndim; ++d) {
+    TMG_REQUIRE(m->dims[d] >= 1, "all dims must be >= 1");
+    TMG_REQUIRE(m->h[d] > 0.0, "all element sizes must be > 0");
+  }
+}
+
+// ----------------------------------------------------------------------------
+// element kernels
+// ----------------------------------------------------------------------------
+__global__ void k_simp(const double* __restrict__ rho, long long n, double p, double e0, double emin,
+                       double* __restrict__ E, unsigned* __restrict__ bad) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double r = rho[i];
+  if (!(r >= 0.0 && r <= 1.0)) atomicOr(bad, 1u);
+  E[i] = emin + (e0 - emin) * pow(r, p);
+}
+
+__global__ void k_check_pos(const double* __restrict__ v, long long n, unsigned* __restrict__ bad) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && !(v[i] > 0.0)) atomicOr(bad, 1u);
+}
+
+// ce_e = u_e^T KE u_e ; optional dc_e = -dE/drho ce_e  (optimization.py:106-129)
+template <int DIM>
+__global__ void __launch_bounds__(TPB) k_strain(FineOp<DIM> op, const double* __restrict__ u, long long nelem,
+                                                double* __restrict__ ce, const double* __restrict__ rho,
+                                                double p, double e0, double emin, double* __restrict__ dc) {
+  extern __shared__ double tmg_smem[];
+  op.init(tmg_smem);
+  __syncthreads();
+  constexpr int NN = 1 << DIM, NE = DIM * NN;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= nelem) return;
+  const int ex = (int)(e % op.ne[0]);
+  const long long t = e / op.ne[0];
+  const int ey = (int)(t % op.ne[1]);
+  const int ez = DIM == 3 ? (int)(t / op.ne[1]) : 0;
+  double ue[NE];
+#pragma unroll
+  for (int m = 0; m < NN; ++m) {
+    const long long node = op.L.id(ex + corner_x(m), ey + corner_y(m), DIM == 3 ? ez + corner_z(m) : 0);
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) ue[m * DIM + c] = u[node * DIM + c];
+  }
+  double s = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < NE; ++i) {
+    double ki = 0.0;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) ki += op.ske[i * NE + j] * ue[j];
+    s += ue[i] * ki;
+  }
+  if (ce) ce[e] = s;
+  if (dc) {
+    const double r = rho[e];
+    const double dE = p == 1.0 ? (e0 - emin) : p * (e0 - emin) * pow(r, p - 1.0);
+    dc[e] = -dE * s;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// ABI
+// ----------------------------------------------------------------------------
+extern "C" {
+
+const char* tmg_last_error(void) { return g_err.c_str(); }
+int tmg_version(void) { return 100; }
+int64_t tmg_launch_count(void) { return launch_counter().load(); }
+int tmg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int tmg_element_stiffness(const tmg_mesh_desc* mesh, double E, double nu, double* ke_host) {
+  ABI_BEGIN
+  check_mesh(mesh);
+  TMG_REQUIRE(nu >= 0.0 && nu < 0.5, "nu must be in [0, 0.5)");
+  TMG_REQUIRE(E > 0.0, "E must be positive");
+  auto ke = element_stiffness(mesh->ndim, mesh->h, E, nu);
+  std::memcpy(ke_host, ke.data(), ke.size() * sizeof(double));
+  ABI_END
+}
+
+int tmg_simp_modulus(const double* rho_dev, int64_t n, double penalty, double e0, double emin, double* E_dev,
+                     void* stream) {
+  ABI_BEGIN
+  require_device();
+  DevBuf<unsigned> bad;
+  bad.alloc(1, S(stream));
+  bad.zero(S(stream));
+  if (n > 0) { k_simp<<<grid_for(n), TPB, 0, S(stream)>>>(rho_dev, n, penalty, e0, emin, E_dev, bad.get()); ::tmg::note_launch(); }
+  unsigned hb = 0;
+  TMG_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, S(stream)));
+  TMG_CUDA(cudaStreamSynchronize(S(stream)));
+  TMG_REQUIRE(hb == 0, "rho must lie in [0, 1]");
+  ABI_END
+}
+
+int tmg_operator_create(const tmg_mesh_desc* mesh, const double* element_moduli_dev, const int64_t* fixed_dofs_host,
+                        int64_t n_fixed, double nu, void* stream, tmg_operator** out) {
+  ABI_BEGIN
+  check_mesh(mesh);
+  TMG_REQUIRE(nu >= 0.0 && nu < 0.5, "nu must be in [0, 0.5)");
+  require_device();
+  cudaStream_t s = S(stream);
+  auto K = std::make_unique<tmg_operator>();
+  Operator& o = K->op;
+  o.dim = mesh->ndim;
+  for (int d = 0; d < 3; ++d) {
+    o.ne[d] = d < o.dim ? mesh->dims[d] : 1;
+    o.h[d] = d < o.dim ? mesh->h[d] : 1.0;
+    o.L.nn[d] = d < o.dim ? mesh->dims[d] + 1 : 1;
+  }
+  o.L.n = (long long)o.L.nn[0] * o.L.nn[1] * o.L.nn[2];
+  o.nelem = (long long)o.ne[0] * o.ne[1] * (o.dim == 3 ? o.ne[2] : 1);
+  o.ndof = o.L.n * o.dim;
+  o.nu = nu;
+  o.ke_host = element_stiffness(o.dim, o.h, 1.0, nu);
+  std::vector<uint8_t> mask(o.L.n, (uint8_t)((1u << o.dim) - 1u));
+  for (int64_t t = 0; t < n_fixed; ++t) {
+    const int64_t d = fixed_dofs_host[t];
+    TMG_REQUIRE(d >= 0 && d < o.ndof, "fixed dof index out of range");
+    mask[d / o.dim] &= (uint8_t)~(1u << (d % o.dim));
+  }
+  o.E.alloc(o.nelem, s);
+  o.ke.alloc(o.ke_host.size(), s);
+  o.mask.alloc(o.L.n, s);
+  TMG_CUDA(cudaMemcpyAsync(o.E.get(), element_moduli_dev, o.nelem * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(o.ke.get(), o.ke_host.data(), o.ke_host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(o.mask.get(), mask.data(), mask.size(), cudaMemcpyHostToDevice, s));
+  DevBuf<unsigned> bad;
+  bad.alloc(1, s);
+  bad.zero(s);
+  k_check_pos<<<grid_for(o.nelem), TPB, 0, s>>>(o.E.get(), o.nelem, bad.get()); ::tmg::note_launch();
+  unsigned hb = 0;
+  TMG_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));  // also makes the pageable H2D sources safe to release
+  TMG_REQUIRE(hb == 0, "element moduli must be positive");
+  *out = K.release();
+  ABI_END
+}
+
+int tmg_operator_destroy(tmg_operator* op) {
+  ABI_BEGIN
+  delete op;
+  ABI_END
+}
+
+int64_t tmg_operator_size(const tmg_operator* op) { return op ? op->op.ndof : -1; }
+
+int tmg_operator_apply(tmg_operator* K, const double* x, double* y, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K, "operator is NULL");
+  const Operator& o = K->op;
+  if (o.dim == 2) {
+    auto f = o.fine<2>();
+    k_apply<2, FineOp<2>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, x, y); ::tmg::note_launch();
+  } else {
+    auto f = o.fine<3>();
+    k_apply<3, FineOp<3>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, x, y); ::tmg::note_launch();
+  }
+  TMG_CUDA(cudaGetLastError());
+  ABI_END
+}
+
+int tmg_operator_diagonal(tmg_operator* K, double* d, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K, "operator is NULL");
+  const Operator& o = K->op;
+  DevBuf<unsigned> bad;
+  bad.alloc(1, S(stream));
+  bad.zero(S(stream));
+  if (o.dim == 2) {
+    auto f = o.fine<2>();
+    k_diag<2, FineOp<2>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
+  } else {
+    auto f = o.fine<3>();
+    k_diag<3, FineOp<3>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
+  }
+  TMG_CUDA(cudaGetLastError());
+  ABI_END
+}
+
+static SmootherCfg to_cfg(const tmg_smoother_desc* d) {
+  SmootherCfg c;
+  if (d) {
+    c.kind = d->kind;
+    c.weight = d->weight;
+    c.degree = d->inner_iterations;
+    c.lanczos_steps = d->lanczos_steps > 0 ? d->lanczos_steps : 10;
+    c.seed = d->seed;
+  }
+  TMG_REQUIRE(c.kind >= 0 && c.kind <= 2, "unknown smoother kind");
+  TMG_REQUIRE(c.weight > 0.0 && c.weight <= 1.0, "smoother weight must be in (0, 1]");
+  TMG_REQUIRE(c.degree >= 1, "inner_iterations must be >= 1");
+  return c;
+}
+
+int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels, const tmg_smoother_desc* smoother,
+                  int32_t n_pre, int32_t n_post, void* stream, tmg_hierarchy** out) {
+  ABI_BEGIN
+  TMG_REQUIRE(K, "operator is NULL");
+  TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
+  const SmootherCfg c = to_cfg(smoother);
+  auto H = std::make_unique<tmg_hierarchy>();
+  H->K = K;
+  if (K->op.dim == 2)
+    H->h = build_gmg<2>(K->op, coarse_max_dofs, max_levels, c, n_pre, n_post, S(stream));
+  else
+    H->h = build_gmg<3>(K->op, coarse_max_dofs, max_levels, c, n_pre, n_post, S(stream));
+  *out = H.release();
+  ABI_END
+}
+
+int tmg_hierarchy_destroy(tmg_hierarchy* h) {
+  ABI_BEGIN
+  delete h;
+  ABI_END
+}
+
+int tmg_hierarchy_num_levels(const tmg_hierarchy* h) { return h ? (int)h->h->lv.size() : -1; }
+
+int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_info* info) {
+  ABI_BEGIN
+  TMG_REQUIRE(h, "hierarchy is NULL");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  const Level& l = *h->h->lv[level];
+  const int D = h->h->dim;
+  info->size = l.ndof;
+  info->provenance = h->h->provenance[level];
+  if (level == h->h->last() && level > 0) {
+    info->storage = 3;
+    info->nonzeros = l.ndof * l.ndof;
+  } else if (l.fine) {
+    info->storage = 0;
+    info->nonzeros = l.op->nelem;
+  } else {
+    info->storage = 1;
+    info->nonzeros = (D == 2 ? 9 : 27) * (long long)D * D * l.L.n;
+  }
+  ABI_END
+}
+
+int tmg_hierarchy_vcycle(tmg_hierarchy* h, int32_t level, const double* b, double* x, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h, "hierarchy is NULL");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  if (h->h->dim == 2) vcycle<2>(*h->h, level, b, x, S(stream));
+  else vcycle<3>(*h->h, level, b, x, S(stream));
+  TMG_CUDA(cudaGetLastError());
+  ABI_END
+}
+
+int tmg_hierarchy_level_apply(tmg_hierarchy* h, int32_t level, const double* x, double* y, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h, "hierarchy is NULL");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  if (h->h->dim == 2) level_apply<2>(*h->h->lv[level], x, y, S(stream));
+  else level_apply<3>(*h->h->lv[level], x, y, S(stream));
+  TMG_CUDA(cudaGetLastError());
+  ABI_END
+}
+
+int tmg_hierarchy_level_lmax(tmg_hierarchy* h, int32_t level, double* lmax, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h, "hierarchy is NULL");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  const Level& l = *h->h->lv[level];
+  *lmax = std::nan("");
+  if (l.lmax.get()) {
+    TMG_CUDA(cudaMemcpyAsync(lmax, l.lmax.get(), sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    TMG_CUDA(cudaStreamSynchronize(S(stream)));
+  }
+  ABI_END
+}
+
+int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, double* ms, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h && reps > 0, "hierarchy is NULL or reps <= 0");
+  if (level < 0 || level >= h->h->last()) throw Error(TMG_ERANGE, "level has no smoother");
+  cudaStream_t s = S(stream);
+  cudaEvent_t a, b;
+  TMG_CUDA(cudaEventCreate(&a));
+  TMG_CUDA(cudaEventCreate(&b));
+  auto run = [&](auto dimtag) {
+    constexpr int DIM = decltype(dimtag)::value;
+    Hierarchy& H = *h->h;
+    Level& l = *H.lv[level];
+    with_op<DIM>(l, [&](auto o) {
+      for (int r = 0; r < reps + 1; ++r) {
+        if (r == 1) TMG_CUDA(cudaEventRecord(a, s));
+        if (H.sm.kind == SM_CHEBYSHEV)
+          k_cheb<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.r.get(), l.p.get(), l.dinv.get(),
+                                                                           l.coef.get(), 1, 0, l.x.get(), l.pt.get(),
+                                                                           l.rt.get());
+        else
+          k_jacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.x.get(), l.b.get(), l.dinv.get(),
+                                                                             H.sm.weight, l.xt.get());
+      }
+    });
+  };
+  if (h->h->dim == 2) run(std::integral_constant<int, 2>());
+  else run(std::integral_constant<int, 3>());
+  TMG_CUDA(cudaEventRecord(b, s));
+  TMG_CUDA(cudaEventSynchronize(b));
+  float t = 0.f;
+  TMG_CUDA(cudaEventElapsedTime(&t, a, b));
+  *ms = t / reps;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  ABI_END
+}
+
+int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x, int32_t use_x0,
+                  const tmg_solve_desc* cfg, double* hist, tmg_solve_record* rec, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K && cfg, "operator/config is NULL");
+  Hierarchy* H = h ? h->h.get() : nullptr;
+  if (h) TMG_REQUIRE(h->h->lv[0]->op == &K->op, "hierarchy was built for a different operator");
+  std::unique_ptr<PcgCtx>& slot = h ? h->pcg : K->pcg;
+  PcgResult r = K->op.dim == 2
+                    ? pcg_solve<2>(slot, K->op, H, b, x, use_x0 != 0, cfg->rtol, cfg->max_iterations, S(stream))
+                    : pcg_solve<3>(slot, K->op, H, b, x, use_x0 != 0, cfg->rtol, cfg->max_iterations, S(stream));
+  if (rec) {
+    rec->iterations = r.iterations;
+    rec->converged = r.converged;
+    rec->initial_residual = r.r0;
+    rec->final_residual = r.rfinal;
+    rec->solve_ms = r.ms;
+  }
+  if (hist) std::memcpy(hist, r.hist.data(), r.hist.size() * sizeof(double));
+  ABI_END
+}
+
+static void launch_strain(const Operator& o, const double* u, double* ce, const double* rho, double p, double e0,
+                          double emin, double* dc, cudaStream_t s) {
+  if (o.dim == 2) {
+    auto f = o.fine<2>();
+    k_strain<2><<<grid_for(o.nelem), TPB, smem_of(f), s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
+  } else {
+    auto f = o.fine<3>();
+    k_strain<3><<<grid_for(o.nelem), TPB, smem_of(f), s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
+  }
+  TMG_CUDA(cudaGetLastError());
+}
+
+int tmg_strain_energy(tmg_operator* K, const double* u, double* ce, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K, "operator is NULL");
+  launch_strain(K->op, u, ce, nullptr, 1.0, 1.0, 0.0, nullptr, S(stream));
+  ABI_END
+}
+
+int tmg_compliance_sensitivity(tmg_operator* K, const double* rho, const double* f, const double* u, double penalty,
+                               double e0, double emin, double* dc, double* compliance, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K, "operator is NULL");
+  cudaStream_t s = S(stream);
+  launch_strain(K->op, u, nullptr, rho, penalty, e0, emin, dc, s);
+  if (compliance) {
+    RedSlot r;
+    r.alloc(1184, s);
+    k_dot<<<std::min<unsigned>(grid_for(K->op.ndof), 1184), TPB, 0, s>>>(f, u, K->op.ndof, r.red()); ::tmg::note_launch();
+    TMG_CUDA(cudaMemcpyAsync(compliance, r.res.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    TMG_CUDA(cudaStreamSynchronize(s));
+  }
+  ABI_END
+}
+
+int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host, const int64_t* fixed_host,
+                              int64_t n_fixed, const double* f_host, double penalty, double e0, double emin,
+                              double nu, const tmg_mg_desc* mg, const tmg_solve_desc* cfg, double* u_host,
+                              double* dc_host, double* compliance_host, tmg_solve_record* rec) {
+  ABI_BEGIN
+  check_mesh(mesh);
+  TMG_REQUIRE(mg && cfg, "mg/solve descriptor is NULL");
+  TMG_REQUIRE(mg->strategy == 0, "only strategy 0 (gmg) is available through this entry point");
+  require_device();
+  cudaStream_t s;
+  TMG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  } guard{s};
+  long long nel = 1, nnode = 1;
+  for (int d = 0; d < mesh->ndim; ++d) { nel *= mesh->dims[d]; nnode *= mesh->dims[d] + 1; }
+  const long long ndof = nnode * mesh->ndim;
+  DevBuf<double> rho, E, f, u, dc;
+  rho.alloc(nel, s); E.alloc(nel, s); f.alloc(ndof, s); u.alloc(ndof, s); dc.alloc(nel, s);
+  TMG_CUDA(cudaMemcpyAsync(rho.get(), rho_host, nel * sizeof(double), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(f.get(), f_host, ndof * sizeof(double), cudaMemcpyHostToDevice, s));
+  int rc = tmg_simp_modulus(rho.get(), nel, penalty, e0, emin, E.get(), s);
+  if (rc) return rc;
+  tmg_operator* K = nullptr;
+  rc = tmg_operator_create(mesh, E.get(), fixed_host, n_fixed, nu, s, &K);
+  if (rc) return rc;
+  std::unique_ptr<tmg_operator> Kg(K);
+  tmg_hierarchy* H = nullptr;
+  rc = tmg_gmg_build(K, mg->coarse_max_dofs, mg->max_levels, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+  if (rc) return rc;
+  std::unique_ptr<tmg_hierarchy> Hg(H);
+  rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);
+  if (rc) return rc;
+  rc = tmg_compliance_sensitivity(K, rho.get(), f.get(), u.get(), penalty, e0, emin, dc.get(), compliance_host, s);
+  if (rc) return rc;
+  TMG_CUDA(cudaMemcpyAsync(u_host, u.get(), ndof * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaMemcpyAsync(dc_host, dc.get(), nel * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  ABI_END
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// Common device/host plumbing for the B200 MG-PCG library.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tmg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TMG_CUDA(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::tmg::Error(-3, std::string(#x) + " -> " + cudaGetErrorString(e_) + " @" + \
+                                 __FILE__ + ":" + std::to_string(__LINE__));           \
+  } while (0)
+
+#define TMG_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) throw ::tmg::Error(-1, msg); \
+  } while (0)
+
+constexpr int TPB = 256;  // threads per block for node-parallel kernels
+
+// Count of this library's kernel launches (graph replays included), for the
+// bench's gpu_launches claim.
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+inline void note_launch(long long n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
+
+inline unsigned grid_for(long long n, int tpb = TPB) {
+  long long g = (n + tpb - 1) / tpb;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+// Stream-ordered device buffer (cudaMallocAsync) -- setup never forces a device sync.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) TMG_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+  }
+  void zero(cudaStream_t st) {
+    if (n) TMG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+// Node lattice of a structured level: nodes lexicographic with x fastest
+// (reference mesh.py:65 node_index).  In 2D nn[2] == 1.
+struct Lat {
+  int nn[3];
+  long long n;
+  __host__ __device__ long long id(int i, int j, int k) const {
+    return i + (long long)nn[0] * (j + (long long)nn[1] * k);
+  }
+  __device__ void ijk(long long node, int& i, int& j, int& k) const {
+    i = (int)(node % nn[0]);
+    long long t = node / nn[0];
+    j = (int)(t % nn[1]);
+    k = (int)(t / nn[1]);
+  }
+  __host__ __device__ bool inside(int i, int j, int k) const {
+    return i >= 0 && i < nn[0] && j >= 0 && j < nn[1] && k >= 0 && k < nn[2];
+  }
+};
+
+// Deterministic grid-wide reduction: per-block partials, the last block to
+// finish sums them in a fixed order and publishes one scalar (no atomics on the
+// value itself, so results are bitwise reproducible run to run).
+struct Red {
+  double* partials;   // >= gridDim.x entries
+  unsigned* counter;  // zero-initialised, reset by the last block
+  double* result;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-level sum (blockDim.x multiple of 32, <= 1024). Valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) ws[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = (threadIdx.x < nw) ? ws[threadIdx.x] : 0.0;
+  if (w == 0) v = warp_sum(v);
+  return v;
+}
+
+// Every thread of every block must call this (uniform control flow).
+__device__ __forceinline__ void grid_reduce(double v, const Red& r) {
+  __shared__ bool last;
+  double b = block_sum(v);
+  if (threadIdx.x == 0) {
+    r.partials[blockIdx.x] = b;
+    __threadfence();
+    unsigned done = atomicAdd(r.counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+      s += ((volatile double*)r.partials)[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) {
+      *r.result = s;
+      *r.counter = 0u;
+    }
+  }
+}
+
+// A reduction slot with its own storage.
+struct RedSlot {
+  DevBuf<double> part;
+  DevBuf<unsigned> cnt;
+  DevBuf<double> res;
+  void alloc(unsigned max_blocks, cudaStream_t s) {
+    part.alloc(max_blocks, s);
+    cnt.alloc(1, s);
+    cnt.zero(s);
+    res.alloc(1, s);
+    res.zero(s);
+  }
+  Red red() const { return Red{part.get(), cnt.get(), res.get()}; }
+};
+
+}  // namespace tmg

@@ -1,0 +1,165 @@
+// Coarsest-level direct solve (reference: splu of the coarsest operator at build
+// time, multigrid.py:256).  On the B200 the coarse operator is inverted once at
+// setup with a blocked Gauss-Jordan sweep (NB-column pivot blocks, rank-NB
+// trailing updates in register-tiled fp64 tiles), and every V-cycle then applies
+// the explicit inverse as one bandwidth-bound GEMV instead of two latency-bound
+// triangular solves.
+#pragma once
+#include "tmg_common.cuh"
+
+namespace tmg {
+
+constexpr int GJ_NB = 32;
+
+// In-place Gauss-Jordan of the kb x kb pivot block; writes D = A_KK^-1.
+__global__ void __launch_bounds__(1024) k_gj_pivot(const double* __restrict__ A, long long n, long long k0, int kb,
+                                                   double* __restrict__ D, unsigned* __restrict__ bad) {
+  __shared__ double M[GJ_NB][GJ_NB + 1];
+  const int i = threadIdx.y, j = threadIdx.x;
+  const bool in = i < kb && j < kb;
+  if (in) M[i][j] = A[(k0 + i) * n + k0 + j];
+  __syncthreads();
+  for (int p = 0; p < kb; ++p) {
+    double piv = M[p][p];
+    double mip = in ? M[i][p] : 0.0, mpj = in ? M[p][j] : 0.0, mij = in ? M[i][j] : 0.0;
+    __syncthreads();
+    if (!(piv > 0.0)) {
+      if (i == 0 && j == 0) atomicOr(bad, 1u);
+      piv = 1.0;
+    }
+    const double d = 1.0 / piv;
+    if (in) {
+      if (i == p && j == p) M[i][j] = d;
+      else if (i == p) M[i][j] = mpj * d;
+      else if (j == p) M[i][j] = -mip * d;
+      else M[i][j] = mij - mip * mpj * d;
+    }
+    __syncthreads();
+  }
+  if (in) D[i * GJ_NB + j] = M[i][j];
+}
+
+// RowP[r][j] = sum_c D[r][c] A[k0+c][j]  (all j);  ColP[i][c] = A[i][k0+c]
+__global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A, long long n, long long k0, int kb,
+                                                   const double* __restrict__ D, double* __restrict__ RowP,
+                                                   double* __restrict__ ColP) {
+  __shared__ double Ds[GJ_NB * GJ_NB];
+  for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t] = D[t];
+  __syncthreads();
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double col[GJ_NB];
+#pragma unroll
+  for (int c = 0; c < GJ_NB; ++c) col[c] = c < kb ? A[(k0 + c) * n + j] : 0.0;
+#pragma unroll 4
+  for (int r = 0; r < kb; ++r) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < GJ_NB; ++c) s += Ds[r * GJ_NB + c] * col[c];
+    RowP[r * n + j] = s;
+  }
+  for (int c = 0; c < kb; ++c) ColP[j * GJ_NB + c] = A[j * n + k0 + c];
+}
+
+// 64x64 output tile per block, 256 threads x (4x4) outputs.
+__global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ A, long long n, long long k0, int kb,
+                                                   const double* __restrict__ D, const double* __restrict__ RowP,
+                                                   const double* __restrict__ ColP) {
+  __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[i0+ii][c]
+  __shared__ double Rs[GJ_NB][64 + 1];  // Rs[c][jj] = RowP[c][j0+jj]
+  __shared__ double Ds[GJ_NB][GJ_NB + 1];
+  const long long i0 = blockIdx.y * 64LL, j0 = blockIdx.x * 64LL;
+  for (int t = threadIdx.x; t < GJ_NB * 64; t += blockDim.x) {
+    const int c = t / 64, q = t % 64;
+    const long long gi = i0 + q, gj = j0 + q;
+    Cs[c][q] = (c < kb && gi < n) ? ColP[gi * GJ_NB + c] : 0.0;
+    Rs[c][q] = (c < kb && gj < n) ? RowP[c * n + gj] : 0.0;
+  }
+  for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t / GJ_NB][t % GJ_NB] = D[t];
+  __syncthreads();
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int c = 0; c < kb; ++c) {
+    double cv[4], rv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) cv[a] = Cs[c][ty + 16 * a];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) rv[b] = Rs[c][tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] += cv[a] * rv[b];
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const long long gi = i0 + ty + 16 * a;
+    if (gi >= n) continue;
+    const bool iK = gi >= k0 && gi < k0 + kb;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const long long gj = j0 + tx + 16 * b;
+      if (gj >= n) continue;
+      const bool jK = gj >= k0 && gj < k0 + kb;
+      double* dst = &A[gi * n + gj];
+      if (!iK && !jK) {
+        *dst -= acc[a][b];
+      } else if (iK && !jK) {
+        *dst = Rs[gi - k0][tx + 16 * b];
+      } else if (!iK && jK) {
+        double s = 0.0;
+        for (int c = 0; c < kb; ++c) s += Cs[c][ty + 16 * a] * Ds[c][gj - k0];
+        *dst = -s;
+      } else {
+        *dst = Ds[gi - k0][gj - k0];
+      }
+    }
+  }
+}
+
+// y = Ainv b: one warp per row, coalesced row reads.
+__global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A, long long n,
+                                                   const double* __restrict__ b, double* __restrict__ y) {
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* a = A + row * n;
+  double s = 0.0;
+  for (long long j = lane; j < n; j += 32) s += a[j] * b[j];
+  s = warp_sum(s);
+  if (lane == 0) y[row] = s;
+}
+
+// Dense SPD inverse on the device (setup; stream-ordered, no host sync).
+struct DenseInverse {
+  long long n = 0;
+  DevBuf<double> A;  // holds the inverse after build()
+  DevBuf<double> D, RowP, ColP;
+  DevBuf<unsigned> bad;
+  void build(cudaStream_t s) {
+    D.alloc(GJ_NB * GJ_NB, s);
+    RowP.alloc((size_t)GJ_NB * n, s);
+    ColP.alloc((size_t)GJ_NB * n, s);
+    bad.alloc(1, s);
+    bad.zero(s);
+    const unsigned tiles = (unsigned)((n + 63) / 64);
+    for (long long k0 = 0; k0 < n; k0 += GJ_NB) {
+      const int kb = (int)std::min<long long>(GJ_NB, n - k0);
+      k_gj_pivot<<<1, dim3(GJ_NB, GJ_NB), 0, s>>>(A.get(), n, k0, kb, D.get(), bad.get()); ::tmg::note_launch();
+      k_gj_panels<<<grid_for(n), 256, 0, s>>>(A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+      k_gj_update<<<dim3(tiles, tiles), 256, 0, s>>>(A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+    }
+    TMG_CUDA(cudaGetLastError());
+    RowP.release();
+    ColP.release();
+    D.release();
+  }
+  void apply(const double* b, double* y, cudaStream_t s) const {
+    k_gemv_rows<<<grid_for(n * 32), 256, 0, s>>>(A.get(), n, b, y); ::tmg::note_launch();
+  }
+};
+
+}  // namespace tmg

@@ -1,0 +1,437 @@
+// Geometric multigrid hierarchy (reference multigrid.py:200-336) on the device:
+// level 0 is the matrix-free FineOp, coarser levels are Galerkin stencils built by
+// k_rap, the coarsest is inverted densely.  The V-cycle (multigrid.py:231) is an
+// enqueue-only host routine, so it can be captured into a CUDA graph.
+#pragma once
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <memory>
+
+#include "tmg_dense.cuh"
+#include "tmg_ke.h"
+#include "tmg_ops.cuh"
+
+namespace tmg {
+
+enum SmootherKind { SM_JACOBI = 0, SM_BLOCK_JACOBI = 1, SM_CHEBYSHEV = 2 };
+
+struct SmootherCfg {
+  int kind = SM_JACOBI;
+  double weight = 0.5;
+  int degree = 2;
+  int lanczos_steps = 10;
+  uint64_t seed = 0;
+};
+
+// ----------------------------------------------------------------------------
+// small vector kernels
+// ----------------------------------------------------------------------------
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, long long n, Red red) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s += a[i] * b[i];
+  grid_reduce(s, red);
+}
+__global__ void k_scale_vec(const double* __restrict__ b, const double* __restrict__ d, double w,
+                            double* __restrict__ x, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = w * (d[i] * b[i]);
+}
+template <int DIM>
+__global__ void k_bscale_vec(const double* __restrict__ b, const double* __restrict__ binv, double w,
+                             double* __restrict__ x, long long nnodes) {
+  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (node >= nnodes) return;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) s += binv[node * DIM * DIM + a * DIM + c] * b[node * DIM + c];
+    x[node * DIM + a] = w * s;
+  }
+}
+__global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv, double* __restrict__ dsq, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dinv[i] = 1.0 / d[i];
+  if (dsq) dsq[i] = sqrt(1.0 / d[i]);
+}
+// splitmix64 start vector, bit-identical to oracle.splitmix_uniform
+__global__ void k_splitmix(double* __restrict__ v, long long n, unsigned long long seed) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long G = 0x9E3779B97F4A7C15ULL;
+  unsigned long long z = seed * G + (unsigned long long)(i + 1) * G;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z = z ^ (z >> 31);
+  v[i] = (double)(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+__global__ void k_div_sqrt(double* __restrict__ v, const double* __restrict__ s2, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = v[i] / sqrt(*s2);
+}
+// w -= a v + b vprev  (b from beta2 slot j-1 or 0)
+__global__ void k_lz_orth(double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ vp,
+                          const double* __restrict__ alpha, const double* __restrict__ beta2, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = *alpha;
+  const double b = beta2 ? sqrt(*beta2) : 0.0;
+  w[i] = b != 0.0 ? w[i] - a * v[i] - b * vp[i] : w[i] - a * v[i];
+}
+__global__ void k_lz_next(double* __restrict__ v, double* __restrict__ vp, const double* __restrict__ w,
+                          const double* __restrict__ beta2, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  vp[i] = v[i];
+  v[i] = w[i] / sqrt(*beta2);
+}
+// Largest eigenvalue of the Lanczos tridiagonal by Sturm bisection, then the
+// Chebyshev step coefficients on [0.1, 1.1] * lambda (multigrid.py:129-149).
+__global__ void k_lz_finish(const double* __restrict__ alpha, const double* __restrict__ beta2, int steps,
+                            int degree, double* __restrict__ coef, double* __restrict__ lmax_out) {
+  int m = steps;
+  for (int j = 0; j < steps; ++j)
+    if (!(sqrt(beta2[j]) > 1e-300)) { m = j + 1; break; }
+  double lo = 1e300, hi = -1e300;
+  for (int j = 0; j < m; ++j) {
+    const double bl = j > 0 ? sqrt(beta2[j - 1]) : 0.0, br = j < m - 1 ? sqrt(beta2[j]) : 0.0;
+    lo = fmin(lo, alpha[j] - bl - br);
+    hi = fmax(hi, alpha[j] + bl + br);
+  }
+  for (int it = 0; it < 200; ++it) {  // count of eigenvalues < x via LDL^T pivots
+    const double x = 0.5 * (lo + hi);
+    if (x == lo || x == hi) break;
+    int cnt = 0;
+    double q = 1.0;
+    for (int j = 0; j < m; ++j) {
+      const double b2 = j > 0 ? beta2[j - 1] : 0.0;
+      q = (alpha[j] - x) - (j > 0 ? b2 / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0.0) ++cnt;
+    }
+    if (cnt == m) hi = x; else lo = x;
+  }
+  const double lam = hi;
+  *lmax_out = lam;
+  const double a = 0.1 * lam, b = 1.1 * lam, theta = 0.5 * (b + a), delta = 0.5 * (b - a);
+  double al = 0.0, be = 0.0;
+  for (int i = 0; i < degree; ++i) {
+    if (i == 0) { al = 1.0 / theta; be = 0.0; }
+    else { be = (delta * al / 2.0) * (delta * al / 2.0); al = 1.0 / (theta - be / al); }
+    coef[2 * i] = al;
+    coef[2 * i + 1] = be;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// the stiffness operator K(rho) (mesh.py:327)
+// ----------------------------------------------------------------------------
+struct Operator {
+  int dim = 2;
+  Lat L{};
+  int ne[3] = {1, 1, 1};
+  double h[3] = {1, 1, 1};
+  double nu = 0.3;
+  long long nelem = 0, ndof = 0;
+  DevBuf<double> E, ke;
+  DevBuf<uint8_t> mask;
+  std::vector<double> ke_host;
+  template <int DIM>
+  FineOp<DIM> fine() const {
+    FineOp<DIM> o;
+    o.L = L;
+    for (int d = 0; d < 3; ++d) o.ne[d] = ne[d];
+    o.E = E.get();
+    o.mask = mask.get();
+    o.ke_g = ke.get();
+    o.ske = nullptr;
+    return o;
+  }
+};
+
+// ----------------------------------------------------------------------------
+// levels
+// ----------------------------------------------------------------------------
+struct Level {
+  bool fine = false;  // level operator is the matrix-free FineOp
+  Lat L{};
+  long long ndof = 0;
+  const Operator* op = nullptr;  // for fine levels
+  DevBuf<double> A;              // stencil storage (coarse geometric levels)
+  DevBuf<double> diag, dinv, dsq, binv;
+  DevBuf<double> b, x, xt, r, rt, p, pt;
+  Coarsening T{};  // to the next level
+  DevBuf<double> coef, lmax;  // Chebyshev
+};
+
+struct Hierarchy {
+  int dim = 2;
+  int n_pre = 1, n_post = 1;
+  SmootherCfg sm;
+  std::vector<std::unique_ptr<Level>> lv;
+  DenseInverse coarse;
+  std::vector<int> provenance;
+  RedSlot red;  // scratch reduction for setup
+  int last() const { return (int)lv.size() - 1; }
+};
+
+template <int DIM, class F>
+void with_op(const Level& l, F&& f) {
+  if (l.fine) {
+    f(l.op->template fine<DIM>());
+  } else {
+    StencilOp<DIM> o;
+    o.L = l.L;
+    o.A = l.A.get();
+    f(o);
+  }
+}
+
+template <class Op>
+inline size_t smem_of(const Op&) { return Op::SMEM * sizeof(double); }
+
+template <int DIM>
+void level_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
+  with_op<DIM>(l, [&](auto o) {
+    k_apply<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, x, y); ::tmg::note_launch();
+  });
+}
+
+// Lanczos bound + Chebyshev coefficients for a level (device only)
+template <int DIM>
+void chebyshev_setup(Hierarchy& H, Level& l, cudaStream_t s) {
+  const int m = H.sm.lanczos_steps;
+  DevBuf<double> v, vp, w, alpha, beta2, nrm;
+  v.alloc(l.ndof, s); vp.alloc(l.ndof, s); w.alloc(l.ndof, s);
+  alpha.alloc(std::max(m, 1), s); beta2.alloc(std::max(m, 1), s); nrm.alloc(1, s);
+  alpha.zero(s); beta2.zero(s);
+  l.coef.alloc(2 * std::max(H.sm.degree, 1), s);
+  l.lmax.alloc(1, s);
+  const unsigned g = grid_for(l.ndof);
+  const unsigned gr = std::min<unsigned>(g, 1184);
+  k_splitmix<<<g, TPB, 0, s>>>(v.get(), l.ndof, (unsigned long long)H.sm.seed); ::tmg::note_launch();
+  Red rn = H.red.red();
+  rn.result = nrm.get();
+  k_dot<<<gr, TPB, 0, s>>>(v.get(), v.get(), l.ndof, rn); ::tmg::note_launch();
+  k_div_sqrt<<<g, TPB, 0, s>>>(v.get(), nrm.get(), l.ndof); ::tmg::note_launch();
+  for (int j = 0; j < m; ++j) {
+    with_op<DIM>(l, [&](auto o) {
+      k_apply_sym<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, v.get(), l.dsq.get(), w.get()); ::tmg::note_launch();
+    });
+    Red ra = H.red.red();
+    ra.result = alpha.get() + j;
+    k_dot<<<gr, TPB, 0, s>>>(w.get(), v.get(), l.ndof, ra); ::tmg::note_launch();
+    k_lz_orth<<<g, TPB, 0, s>>>(w.get(), v.get(), vp.get(), alpha.get() + j, j > 0 ? beta2.get() + j - 1 : nullptr,
+                                l.ndof); ::tmg::note_launch();
+    Red rb = H.red.red();
+    rb.result = beta2.get() + j;
+    k_dot<<<gr, TPB, 0, s>>>(w.get(), w.get(), l.ndof, rb); ::tmg::note_launch();
+    if (j + 1 < m) { k_lz_next<<<g, TPB, 0, s>>>(v.get(), vp.get(), w.get(), beta2.get() + j, l.ndof); ::tmg::note_launch(); }
+  }
+  k_lz_finish<<<1, 1, 0, s>>>(alpha.get(), beta2.get(), m, H.sm.degree, l.coef.get(), l.lmax.get()); ::tmg::note_launch();
+  TMG_CUDA(cudaGetLastError());
+}
+
+template <int DIM>
+void level_setup(Hierarchy& H, Level& l, bool smoother_needed, cudaStream_t s, DevBuf<unsigned>& bad) {
+  const long long nd = l.ndof;
+  l.diag.alloc(nd, s);
+  l.dinv.alloc(nd, s);
+  const bool cheb = H.sm.kind == SM_CHEBYSHEV;
+  if (cheb) l.dsq.alloc(nd, s);
+  if (H.sm.kind == SM_BLOCK_JACOBI) l.binv.alloc(nd * DIM, s);
+  with_op<DIM>(l, [&](auto o) {
+    k_diag<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.diag.get(), l.binv.get(), bad.get()); ::tmg::note_launch();
+  });
+  k_recip<<<grid_for(nd), TPB, 0, s>>>(l.diag.get(), l.dinv.get(), cheb ? l.dsq.get() : nullptr, nd); ::tmg::note_launch();
+  l.b.alloc(nd, s); l.x.alloc(nd, s); l.xt.alloc(nd, s); l.r.alloc(nd, s);
+  if (cheb) { l.rt.alloc(nd, s); l.p.alloc(nd, s); l.pt.alloc(nd, s); }
+  if (cheb && smoother_needed) chebyshev_setup<DIM>(H, l, s);
+}
+
+inline int coarsen1(int d) { return std::max(1, (d + 1) / 2); }
+
+// multigrid.py:276 gmg_level_dims (+ optional level cap)
+inline std::vector<std::array<int, 3>> gmg_plan(int dim, const int* ne, long long coarse_max_dofs, int max_levels) {
+  std::vector<std::array<int, 3>> plan;
+  plan.push_back({ne[0], ne[1], dim == 3 ? ne[2] : 0});
+  while (true) {
+    auto cur = plan.back();
+    long long nodes = 1;
+    bool all1 = true;
+    for (int d = 0; d < dim; ++d) { nodes *= (cur[d] + 1); all1 = all1 && cur[d] <= 1; }
+    if (dim * nodes <= coarse_max_dofs || all1) break;
+    if (max_levels > 0 && (int)plan.size() >= max_levels) break;
+    std::array<int, 3> nx = cur;
+    for (int d = 0; d < dim; ++d) nx[d] = coarsen1(cur[d]);
+    plan.push_back(nx);
+  }
+  return plan;
+}
+
+template <int DIM>
+std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dofs, int max_levels,
+                                     const SmootherCfg& sm, int n_pre, int n_post, cudaStream_t s) {
+  auto H = std::make_unique<Hierarchy>();
+  H->dim = DIM;
+  H->n_pre = n_pre;
+  H->n_post = n_post;
+  H->sm = sm;
+  H->red.alloc(4096, s);
+  DevBuf<unsigned> bad;
+  bad.alloc(1, s);
+  bad.zero(s);
+  auto plan = gmg_plan(DIM, K.ne, coarse_max_dofs, max_levels);
+  const int nl = (int)plan.size();
+  for (int k = 0; k < nl; ++k) {
+    auto l = std::make_unique<Level>();
+    const auto& ed = plan[k];
+    for (int d = 0; d < 3; ++d) l->L.nn[d] = d < DIM ? ed[d] + 1 : 1;
+    l->L.n = (long long)l->L.nn[0] * l->L.nn[1] * l->L.nn[2];
+    l->ndof = l->L.n * DIM;
+    if (k == 0) {
+      l->fine = true;
+      l->op = &K;
+    } else {
+      Level& f = *H->lv[k - 1];
+      Coarsening T;
+      T.F = f.L;
+      T.C = l->L;
+      for (int d = 0; d < 3; ++d) T.co[d] = (d < DIM && plan[k - 1][d] > 1) ? 1 : 0;
+      f.T = T;
+      l->A.alloc((size_t)Slots<DIM>::NS * DIM * DIM * l->L.n, s);
+      with_op<DIM>(f, [&](auto o) {
+        const long long nt = l->L.n * Slots<DIM>::NS;
+        k_rap<DIM, decltype(o)><<<grid_for(nt), TPB, smem_of(o), s>>>(o, T, l->A.get()); ::tmg::note_launch();
+      });
+      TMG_CUDA(cudaGetLastError());
+    }
+    H->provenance.push_back(0);
+    H->lv.push_back(std::move(l));
+  }
+  for (int k = 0; k < nl; ++k) level_setup<DIM>(*H, *H->lv[k], k < nl - 1, s, bad);
+  // coarsest: dense inverse
+  Level& c = *H->lv[nl - 1];
+  H->coarse.n = c.ndof;
+  H->coarse.A.alloc((size_t)c.ndof * c.ndof, s);
+  H->coarse.A.zero(s);
+  with_op<DIM>(c, [&](auto o) {
+    k_to_dense<DIM, decltype(o)><<<grid_for(c.L.n), TPB, smem_of(o), s>>>(o, H->coarse.A.get()); ::tmg::note_launch();
+  });
+  H->coarse.build(s);
+  unsigned hbad = 0, cbad = 0;
+  TMG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaMemcpyAsync(&cbad, H->coarse.bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  if (hbad & 1u) throw Error(-1, "zero diagonal entry; operator not smoothable");
+  if ((hbad & 2u) && sm.kind == SM_BLOCK_JACOBI) throw Error(-1, "singular nodal block in block Jacobi smoother");
+  if (cbad) throw Error(-5, "coarsest operator is not positive definite");
+  return H;
+}
+
+// ----------------------------------------------------------------------------
+// V-cycle (multigrid.py:231), enqueue only
+// ----------------------------------------------------------------------------
+template <int DIM>
+void smooth_jacobi(Hierarchy& H, Level& l, const double* b, double*& cur, int passes, double* const bufs[2],
+                   int& widx, int W, cudaStream_t s) {
+  for (int p = 0; p < passes; ++p) {
+    ++widx;
+    double* dst = ((W - widx) % 2 == 0) ? bufs[0] : bufs[1];
+    if (cur == nullptr) {  // zero start: x = w D^-1 b without a product
+      if (H.sm.kind == SM_BLOCK_JACOBI)
+        k_bscale_vec<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(b, l.binv.get(), H.sm.weight, dst, l.L.n);
+      else
+        k_scale_vec<<<grid_for(l.ndof), TPB, 0, s>>>(b, l.dinv.get(), H.sm.weight, dst, l.ndof);
+      ::tmg::note_launch();
+    } else {
+      with_op<DIM>(l, [&](auto o) {
+        if (H.sm.kind == SM_BLOCK_JACOBI)
+          k_bjacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, cur, b, l.binv.get(), H.sm.weight, dst);
+        else
+          k_jacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, cur, b, l.dinv.get(), H.sm.weight, dst);
+        ::tmg::note_launch();
+      });
+    }
+    cur = dst;
+  }
+}
+
+// Chebyshev passes on x (in place); x_zero: x holds garbage and means 0.
+template <int DIM>
+void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero, int passes, cudaStream_t s) {
+  for (int p = 0; p < passes; ++p) {
+    const double* rin;
+    if (x_zero) {
+      rin = b;
+    } else {
+      with_op<DIM>(l, [&](auto o) {
+        k_residual<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, x, b, l.r.get()); ::tmg::note_launch();
+      });
+      rin = l.r.get();
+    }
+    const double* pin = l.p.get();
+    double* rbuf[2] = {l.rt.get(), l.r.get()};
+    double* pbuf[2] = {l.pt.get(), l.p.get()};
+    for (int i = 0; i < H.sm.degree; ++i) {
+      double* ro = rbuf[i % 2];
+      double* po = pbuf[i % 2];
+      if (ro == rin) ro = rbuf[(i + 1) % 2];
+      if (po == pin) po = pbuf[(i + 1) % 2];
+      with_op<DIM>(l, [&](auto o) {
+        k_cheb<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, rin, pin, l.dinv.get(), l.coef.get(), i,
+                                                                         (x_zero && i == 0) ? 1 : 0, x, po, ro); ::tmg::note_launch();
+      });
+      rin = ro;
+      pin = po;
+    }
+    x_zero = false;
+  }
+}
+
+template <int DIM>
+void vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s) {
+  Level& l = *H.lv[k];
+  if (k == H.last()) {
+    H.coarse.apply(b, xout, s);
+    return;
+  }
+  Level& c = *H.lv[k + 1];
+  double* xcur = nullptr;
+  if (H.sm.kind == SM_CHEBYSHEV) {
+    if (H.n_pre > 0) { smooth_cheb<DIM>(H, l, b, xout, true, H.n_pre, s); xcur = xout; }
+  } else {
+    double* const bufs[2] = {xout, l.xt.get()};
+    int widx = 0;
+    const int W = H.n_pre + H.n_post;
+    smooth_jacobi<DIM>(H, l, b, xcur, H.n_pre, bufs, widx, W, s);
+  }
+  const double* r = b;
+  if (xcur) {
+    with_op<DIM>(l, [&](auto o) {
+      k_residual<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, xcur, b, l.r.get()); ::tmg::note_launch();
+    });
+    r = l.r.get();
+  }
+  k_restrict<DIM><<<grid_for(c.L.n), TPB, 0, s>>>(l.T, r, c.b.get(), nullptr, 0.0, nullptr); ::tmg::note_launch();
+  vcycle<DIM>(H, k + 1, c.b.get(), c.x.get(), s);
+  if (!xcur) {
+    xcur = (H.sm.kind == SM_CHEBYSHEV || H.n_post % 2 == 0) ? xout : l.xt.get();
+    TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
+  }
+  k_prolong_add<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(l.T, c.x.get(), xcur); ::tmg::note_launch();
+  if (H.sm.kind == SM_CHEBYSHEV) {
+    smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);
+  } else {
+    double* const bufs[2] = {xout, l.xt.get()};
+    int widx = H.n_pre;
+    const int W = H.n_pre + H.n_post;
+    smooth_jacobi<DIM>(H, l, b, xcur, H.n_post, bufs, widx, W, s);
+  }
+  if (xcur != xout) TMG_CUDA(cudaMemcpyAsync(xout, xcur, l.ndof * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace tmg

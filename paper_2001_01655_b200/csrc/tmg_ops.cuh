@@ -1,0 +1,528 @@
+// Level operators of the geometric hierarchy and the node-parallel kernels that
+// apply them.  Two operator kinds share one interface:
+//
+//  * FineOp<DIM>:   the level-0 stiffness K(rho) kept matrix-free -- element moduli
+//    (8 B/element) and the unit-modulus element matrix KE staged in shared memory.
+//    A row of K is gathered node-centrically from the 2^DIM elements around the
+//    node, so the product is assembled atomic-free with no colouring pass.  The
+//    symmetric Dirichlet elimination of mesh.py:313 (Z K Z + I_fixed) is applied
+//    on the fly from a per-node free-dof bitmask.
+//  * StencilOp<DIM>: a Galerkin coarse operator P^T A P of a geometric level.  On a
+//    structured grid with bilinear/trilinear P it is exactly a 3^DIM-point nodal
+//    stencil of DIM x DIM blocks, stored structure-of-arrays
+//    A[(slot*DIM*DIM + a*DIM + b) * n_nodes + node] so that a warp reads 32
+//    consecutive doubles per (slot, a, b).  No index arrays are stored.
+//
+// Every kernel maps one thread to one node (x fastest), so vector loads are
+// coalesced along x and neighbour gathers hit the same cache lines.
+#pragma once
+#include "tmg_common.cuh"
+
+namespace tmg {
+
+// local corner numbering of mesh.py:73-102
+__host__ __device__ constexpr int corner_of(int dx, int dy, int dz) { return (dy ? 3 - dx : dx) + 4 * dz; }
+__host__ __device__ constexpr int corner_x(int m) { return ((m & 3) == 1 || (m & 3) == 2) ? 1 : 0; }
+__host__ __device__ constexpr int corner_y(int m) { return (m & 3) >= 2 ? 1 : 0; }
+__host__ __device__ constexpr int corner_z(int m) { return m >> 2; }
+
+template <int DIM>
+struct Slots {  // 3^DIM stencil neighbourhood, slot = (dx+1) + 3(dy+1) + 9(dz+1)
+  static constexpr int NS = DIM == 2 ? 9 : 27;
+  __host__ __device__ static constexpr int dx(int s) { return s % 3 - 1; }
+  __host__ __device__ static constexpr int dy(int s) { return (s / 3) % 3 - 1; }
+  __host__ __device__ static constexpr int dz(int s) { return DIM == 3 ? s / 9 - 1 : 0; }
+  __host__ __device__ static constexpr int of(int x, int y, int z) {
+    return (x + 1) + 3 * (y + 1) + (DIM == 3 ? 9 * (z + 1) : 0);
+  }
+};
+
+// ----------------------------------------------------------------------------
+// vector sources (functors giving the value of the vector being multiplied)
+// ----------------------------------------------------------------------------
+template <int DIM>
+struct VecSrc {
+  const double* __restrict__ v;
+  __device__ double operator()(long long node, int c) const { return v[node * DIM + c]; }
+};
+template <int DIM>
+struct ScaledSrc {  // s .* v
+  const double* __restrict__ v;
+  const double* __restrict__ s;
+  __device__ double operator()(long long node, int c) const {
+    return v[node * DIM + c] * s[node * DIM + c];
+  }
+};
+template <int DIM>
+struct AxpySrc {  // z + beta * p  (beta == 0 -> z; never touches p then)
+  const double* __restrict__ z;
+  const double* __restrict__ p;
+  double beta;
+  __device__ double operator()(long long node, int c) const {
+    const long long i = node * DIM + c;
+    return beta == 0.0 ? z[i] : z[i] + beta * p[i];
+  }
+};
+template <int DIM>
+struct ChebSrc {  // dinv .* r + beta * p
+  const double* __restrict__ r;
+  const double* __restrict__ p;
+  const double* __restrict__ dinv;
+  double beta;
+  __device__ double operator()(long long node, int c) const {
+    const long long i = node * DIM + c;
+    const double z = dinv[i] * r[i];
+    return beta == 0.0 ? z : z + beta * p[i];
+  }
+};
+
+// ----------------------------------------------------------------------------
+// FineOp
+// ----------------------------------------------------------------------------
+template <int DIM>
+struct FineOp {
+  static constexpr int NN = 1 << DIM, NE = DIM * NN, DD = DIM * DIM;
+  static constexpr int SMEM = NE * NE;  // doubles of shared memory needed
+  Lat L;
+  int ne[3];
+  const double* __restrict__ E;
+  const uint8_t* __restrict__ mask;  // bit c set -> dof c of the node is free
+  const double* __restrict__ ke_g;
+  const double* ske;
+
+  __device__ void init(double* smem) {
+    for (int t = threadIdx.x; t < SMEM; t += blockDim.x) smem[t] = ke_g[t];
+    ske = smem;
+  }
+  __device__ bool elem_ok(int ex, int ey, int ez) const {
+    return ex >= 0 && ex < ne[0] && ey >= 0 && ey < ne[1] && (DIM == 2 || (ez >= 0 && ez < ne[2]));
+  }
+  __device__ long long elem_id(int ex, int ey, int ez) const {
+    return ex + (long long)ne[0] * (ey + (long long)ne[1] * ez);
+  }
+
+  // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src
+  template <class Src>
+  __device__ void row(long long node, int i, int j, int k, const Src& src, double out[DIM]) const {
+    constexpr int NS = Slots<DIM>::NS;
+    double xv[NS][DIM];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
+      if (L.inside(ii, jj, kk)) {
+        const long long m = L.id(ii, jj, kk);
+        const unsigned mk = mask[m];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) xv[s][d] = ((mk >> d) & 1u) ? src(m, d) : 0.0;
+      } else {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) xv[s][d] = 0.0;
+      }
+    }
+    double acc[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int ez = 0; ez < (DIM == 3 ? 2 : 1); ++ez)
+#pragma unroll
+      for (int ey = 0; ey < 2; ++ey)
+#pragma unroll
+        for (int ex = 0; ex < 2; ++ex) {
+          const int eI = i - 1 + ex, eJ = j - 1 + ey, eK = DIM == 3 ? k - 1 + ez : 0;
+          if (!elem_ok(eI, eJ, eK)) continue;
+          const double Ee = E[elem_id(eI, eJ, eK)];
+          const int ln = corner_of(1 - ex, 1 - ey, DIM == 3 ? 1 - ez : 0);
+          double t[DIM];
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) t[c] = 0.0;
+#pragma unroll
+          for (int m = 0; m < NN; ++m) {
+            const int s = Slots<DIM>::of(ex - 1 + corner_x(m), ey - 1 + corner_y(m),
+                                         DIM == 3 ? ez - 1 + corner_z(m) : 0);
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+#pragma unroll
+              for (int d = 0; d < DIM; ++d) t[c] += ske[(ln * DIM + c) * NE + m * DIM + d] * xv[s][d];
+          }
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) acc[c] += Ee * t[c];
+        }
+    const unsigned mn = mask[node];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = ((mn >> c) & 1u) ? acc[c] : src(node, c);
+  }
+
+  // block (i -> j) of Z K Z + I_fixed, i and j lattice neighbours (|i-j|_inf <= 1)
+  __device__ void block(int i0, int i1, int i2, int j0, int j1, int j2, double blk[DD]) const {
+#pragma unroll
+    for (int t = 0; t < DD; ++t) blk[t] = 0.0;
+    const int lo0 = max(max(i0, j0) - 1, 0), hi0 = min(min(i0, j0), ne[0] - 1);
+    const int lo1 = max(max(i1, j1) - 1, 0), hi1 = min(min(i1, j1), ne[1] - 1);
+    const int lo2 = DIM == 3 ? max(max(i2, j2) - 1, 0) : 0;
+    const int hi2 = DIM == 3 ? min(min(i2, j2), ne[2] - 1) : 0;
+    for (int ez = lo2; ez <= hi2; ++ez)
+      for (int ey = lo1; ey <= hi1; ++ey)
+        for (int ex = lo0; ex <= hi0; ++ex) {
+          const double Ee = E[elem_id(ex, ey, ez)];
+          const int li = corner_of(i0 - ex, i1 - ey, DIM == 3 ? i2 - ez : 0);
+          const int lj = corner_of(j0 - ex, j1 - ey, DIM == 3 ? j2 - ez : 0);
+#pragma unroll
+          for (int a = 0; a < DIM; ++a)
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) blk[a * DIM + b] += Ee * ske[(li * DIM + a) * NE + lj * DIM + b];
+        }
+    const unsigned mi = mask[L.id(i0, i1, i2)], mj = mask[L.id(j0, j1, j2)];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b)
+        if (!(((mi >> a) & 1u) && ((mj >> b) & 1u))) blk[a * DIM + b] = 0.0;
+    if (i0 == j0 && i1 == j1 && i2 == j2) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+        if (!((mi >> a) & 1u)) blk[a * DIM + a] = 1.0;
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------
+// StencilOp
+// ----------------------------------------------------------------------------
+template <int DIM>
+struct StencilOp {
+  static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
+  static constexpr int SMEM = 0;
+  Lat L;
+  const double* __restrict__ A;
+
+  __device__ void init(double*) {}
+
+  template <class Src>
+  __device__ void row(long long node, int i, int j, int k, const Src& src, double out[DIM]) const {
+    double acc[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
+      if (!L.inside(ii, jj, kk)) continue;
+      const long long m = L.id(ii, jj, kk);
+      double xv[DIM];
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) xv[b] = src(m, b);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) acc[a] += A[(s * DD + a * DIM + b) * L.n + node] * xv[b];
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = acc[c];
+  }
+
+  __device__ void block(int i0, int i1, int i2, int j0, int j1, int j2, double blk[DD]) const {
+    const int s = Slots<DIM>::of(j0 - i0, j1 - i1, DIM == 3 ? j2 - i2 : 0);
+    const long long node = L.id(i0, i1, i2);
+#pragma unroll
+    for (int t = 0; t < DD; ++t) blk[t] = A[(s * DD + t) * L.n + node];
+  }
+};
+
+// ----------------------------------------------------------------------------
+// generic node-parallel kernels
+// ----------------------------------------------------------------------------
+#define TMG_NODE_PROLOGUE                               \
+  extern __shared__ double tmg_smem[];                  \
+  op.init(tmg_smem);                                    \
+  __syncthreads();                                      \
+  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x; \
+  const bool active = node < op.L.n;                    \
+  int ci = 0, cj = 0, ck = 0;                           \
+  if (active) op.L.ijk(node, ci, cj, ck);
+
+// y = A x
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_apply(Op op, const double* __restrict__ x, double* __restrict__ y) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double out[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) y[node * DIM + c] = out[c];
+}
+
+// y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_apply_sym(Op op, const double* __restrict__ v, const double* __restrict__ ds,
+                                                   double* __restrict__ y) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double out[DIM];
+  op.row(node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) y[node * DIM + c] = ds[node * DIM + c] * out[c];
+}
+
+// r = b - A x
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_residual(Op op, const double* __restrict__ x, const double* __restrict__ b,
+                                                  double* __restrict__ r) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double out[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) r[node * DIM + c] = b[node * DIM + c] - out[c];
+}
+
+// xo = x + w D^-1 (b - A x)   (weighted Jacobi, multigrid.py:57)
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_jacobi(Op op, const double* __restrict__ x, const double* __restrict__ b,
+                                                const double* __restrict__ dinv, double w, double* __restrict__ xo) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double out[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    const long long i = node * DIM + c;
+    xo[i] = x[i] + w * (dinv[i] * (b[i] - out[c]));
+  }
+}
+
+// xo = x + w B^-1 (b - A x), B the nodal diagonal blocks (multigrid.py:90)
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_bjacobi(Op op, const double* __restrict__ x, const double* __restrict__ b,
+                                                 const double* __restrict__ binv, double w, double* __restrict__ xo) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double out[DIM], r[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) r[c] = b[node * DIM + c] - out[c];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) s += binv[node * DIM * DIM + a * DIM + c] * r[c];
+    xo[node * DIM + a] = x[node * DIM + a] + w * s;
+  }
+}
+
+// One Chebyshev step (multigrid.py:131 recurrence, SOR solve -> D^-1):
+//   p' = D^-1 r + beta p ; x += alpha p' ; r' = r - alpha A p'
+// alpha/beta of step `step` come from the device coefficient array.
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_cheb(Op op, const double* __restrict__ r, const double* __restrict__ p,
+                                              const double* __restrict__ dinv, const double* __restrict__ coef,
+                                              int step, int x_zero, double* __restrict__ x,
+                                              double* __restrict__ po, double* __restrict__ ro) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
+  ChebSrc<DIM> src{r, p, dinv, beta};
+  double out[DIM];
+  op.row(node, ci, cj, ck, src, out);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    const long long i = node * DIM + c;
+    const double pv = src(node, c);
+    po[i] = pv;
+    x[i] = (x_zero ? 0.0 : x[i]) + alpha * pv;
+    ro[i] = r[i] - alpha * out[c];
+  }
+}
+
+// diagonal / nodal block inverses of a level operator
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_diag(Op op, double* __restrict__ diag, double* __restrict__ binv,
+                                              unsigned* __restrict__ bad) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  double blk[DIM * DIM];
+  op.block(ci, cj, ck, ci, cj, ck, blk);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    diag[node * DIM + c] = blk[c * DIM + c];
+    if (blk[c * DIM + c] == 0.0) atomicOr(bad, 1u);
+  }
+  if (binv) {
+    double inv[DIM * DIM];
+    double det;
+    if (DIM == 2) {
+      det = blk[0] * blk[3] - blk[1] * blk[2];
+      inv[0] = blk[3] / det; inv[1] = -blk[1] / det; inv[2] = -blk[2] / det; inv[3] = blk[0] / det;
+    } else {
+      const double* m = blk;
+      const double c00 = m[4] * m[8] - m[5] * m[7], c01 = m[5] * m[6] - m[3] * m[8], c02 = m[3] * m[7] - m[4] * m[6];
+      det = m[0] * c00 + m[1] * c01 + m[2] * c02;
+      inv[0] = c00 / det; inv[1] = (m[2] * m[7] - m[1] * m[8]) / det; inv[2] = (m[1] * m[5] - m[2] * m[4]) / det;
+      inv[3] = c01 / det; inv[4] = (m[0] * m[8] - m[2] * m[6]) / det; inv[5] = (m[2] * m[3] - m[0] * m[5]) / det;
+      inv[6] = c02 / det; inv[7] = (m[1] * m[6] - m[0] * m[7]) / det; inv[8] = (m[0] * m[4] - m[1] * m[3]) / det;
+    }
+    if (!(fabs(det) >= 1e-300)) atomicOr(bad, 2u);
+#pragma unroll
+    for (int t = 0; t < DIM * DIM; ++t) binv[node * DIM * DIM + t] = inv[t];
+  }
+}
+
+// dense row-major copy of a level operator (small coarsest levels only)
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_to_dense(Op op, double* __restrict__ Ad) {
+  TMG_NODE_PROLOGUE
+  if (!active) return;
+  const long long n = op.L.n * DIM;
+  for (int s = 0; s < Slots<DIM>::NS; ++s) {
+    const int ii = ci + Slots<DIM>::dx(s), jj = cj + Slots<DIM>::dy(s), kk = ck + Slots<DIM>::dz(s);
+    if (!op.L.inside(ii, jj, kk)) continue;
+    double blk[DIM * DIM];
+    op.block(ci, cj, ck, ii, jj, kk, blk);
+    const long long m = op.L.id(ii, jj, kk);
+    for (int a = 0; a < DIM; ++a)
+      for (int b = 0; b < DIM; ++b) Ad[(node * DIM + a) * n + m * DIM + b] = blk[a * DIM + b];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// geometric transfers (multigrid.py:288-315): 1D hat interpolation per axis,
+// Kronecker product with x fastest, identity on axes with one element.
+// ----------------------------------------------------------------------------
+struct Coarsening {
+  Lat F, C;       // fine / coarse node lattices
+  int co[3];      // 1 if the axis is coarsened (fine element count > 1)
+};
+
+// fine candidates of coarse index I on one axis: up to 3 (index, weight)
+__device__ __forceinline__ int fine_of_coarse(int I, int co, int nf, int idx[3], double w[3]) {
+  if (!co) { idx[0] = I; w[0] = 1.0; return 1; }
+  int c = 0;
+  const int base = 2 * I;
+  if (base - 1 >= 0 && base - 1 < nf) { idx[c] = base - 1; w[c] = 0.5; ++c; }
+  if (base < nf) { idx[c] = base; w[c] = 1.0; ++c; }
+  if (base + 1 < nf) { idx[c] = base + 1; w[c] = 0.5; ++c; }
+  return c;
+}
+// coarse parents of fine index i on one axis: up to 2 (index, weight)
+__device__ __forceinline__ int coarse_of_fine(int i, int co, int idx[2], double w[2]) {
+  if (!co) { idx[0] = i; w[0] = 1.0; return 1; }
+  if ((i & 1) == 0) { idx[0] = i >> 1; w[0] = 1.0; return 1; }
+  idx[0] = (i - 1) >> 1; idx[1] = (i + 1) >> 1; w[0] = w[1] = 0.5;
+  return 2;
+}
+
+// bc = P^T r ; optionally the first (zero-start) Jacobi sweep of the coarse level:
+// xc = w * dinvc .* bc
+template <int DIM>
+__global__ void __launch_bounds__(TPB) k_restrict(Coarsening T, const double* __restrict__ r, double* __restrict__ bc,
+                                                  const double* __restrict__ dinvc, double w, double* __restrict__ xc) {
+  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (node >= T.C.n) return;
+  int I, J, K;
+  T.C.ijk(node, I, J, K);
+  int ix[3], iy[3], iz[3];
+  double wx[3], wy[3], wz[3];
+  const int nx = fine_of_coarse(I, T.co[0], T.F.nn[0], ix, wx);
+  const int ny = fine_of_coarse(J, T.co[1], T.F.nn[1], iy, wy);
+  const int nz = DIM == 3 ? fine_of_coarse(K, T.co[2], T.F.nn[2], iz, wz) : 1;
+  if (DIM == 2) { iz[0] = 0; wz[0] = 1.0; }
+  double acc[DIM];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+  for (int c2 = 0; c2 < nz; ++c2)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) {
+        const double ww = wx[a] * wy[b] * wz[c2];
+        const long long f = T.F.id(ix[a], iy[b], iz[c2]);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) acc[c] += ww * r[f * DIM + c];
+      }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    bc[node * DIM + c] = acc[c];
+    if (xc) xc[node * DIM + c] = w * dinvc[node * DIM + c] * acc[c];
+  }
+}
+
+// x += P e
+template <int DIM>
+__global__ void __launch_bounds__(TPB) k_prolong_add(Coarsening T, const double* __restrict__ e, double* __restrict__ x) {
+  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (node >= T.F.n) return;
+  int i, j, k;
+  T.F.ijk(node, i, j, k);
+  int ix[2], iy[2], iz[2];
+  double wx[2], wy[2], wz[2];
+  const int nx = coarse_of_fine(i, T.co[0], ix, wx);
+  const int ny = coarse_of_fine(j, T.co[1], iy, wy);
+  const int nz = DIM == 3 ? coarse_of_fine(k, T.co[2], iz, wz) : 1;
+  if (DIM == 2) { iz[0] = 0; wz[0] = 1.0; }
+  double acc[DIM];
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+  for (int c2 = 0; c2 < nz; ++c2)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) {
+        const double ww = wx[a] * wy[b] * wz[c2];
+        const long long m = T.C.id(ix[a], iy[b], iz[c2]);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) acc[c] += ww * e[m * DIM + c];
+      }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) x[node * DIM + c] += acc[c];
+}
+
+// Galerkin product A_c = P^T A P into stencil storage; one thread per
+// (coarse node, stencil slot).  The fine operator is read through its block()
+// provider, so level 0 is never assembled.
+template <int DIM, class Op>
+__global__ void __launch_bounds__(TPB) k_rap(Op op, Coarsening T, double* __restrict__ Ac) {
+  extern __shared__ double tmg_smem[];
+  op.init(tmg_smem);
+  __syncthreads();
+  constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= T.C.n * NS) return;
+  const int s = (int)(t / T.C.n);
+  const long long node = t - (long long)s * T.C.n;
+  int I0, I1, I2;
+  T.C.ijk(node, I0, I1, I2);
+  const int J0 = I0 + Slots<DIM>::dx(s), J1 = I1 + Slots<DIM>::dy(s), J2 = I2 + Slots<DIM>::dz(s);
+  double acc[DD];
+#pragma unroll
+  for (int q = 0; q < DD; ++q) acc[q] = 0.0;
+  if (T.C.inside(J0, J1, J2)) {
+    int fi[3][3], fj[3][3], ni[3], nj[3];
+    double wi[3][3], wj[3][3];
+    const int Iv[3] = {I0, I1, I2}, Jv[3] = {J0, J1, J2};
+    for (int d = 0; d < 3; ++d) {
+      if (d < DIM) {
+        ni[d] = fine_of_coarse(Iv[d], T.co[d], T.F.nn[d], fi[d], wi[d]);
+        nj[d] = fine_of_coarse(Jv[d], T.co[d], T.F.nn[d], fj[d], wj[d]);
+      } else {
+        ni[d] = nj[d] = 1; fi[d][0] = fj[d][0] = 0; wi[d][0] = wj[d][0] = 1.0;
+      }
+    }
+    double blk[DD];
+    for (int a2 = 0; a2 < ni[2]; ++a2)
+      for (int a1 = 0; a1 < ni[1]; ++a1)
+        for (int a0 = 0; a0 < ni[0]; ++a0) {
+          const double wa = wi[0][a0] * wi[1][a1] * wi[2][a2];
+          for (int b2 = 0; b2 < nj[2]; ++b2) {
+            if (abs(fj[2][b2] - fi[2][a2]) > 1) continue;
+            for (int b1 = 0; b1 < nj[1]; ++b1) {
+              if (abs(fj[1][b1] - fi[1][a1]) > 1) continue;
+              for (int b0 = 0; b0 < nj[0]; ++b0) {
+                if (abs(fj[0][b0] - fi[0][a0]) > 1) continue;
+                const double ww = wa * wj[0][b0] * wj[1][b1] * wj[2][b2];
+                op.block(fi[0][a0], fi[1][a1], fi[2][a2], fj[0][b0], fj[1][b1], fj[2][b2], blk);
+#pragma unroll
+                for (int q = 0; q < DD; ++q) acc[q] += ww * blk[q];
+              }
+            }
+          }
+        }
+  }
+#pragma unroll
+  for (int q = 0; q < DD; ++q) Ac[(s * DD + q) * T.C.n + node] = acc[q];
+}
+
+}  // namespace tmg

@@ -1,0 +1,173 @@
+"""Multigrid hierarchies on the B200 (mirrors reference multigrid.py).
+
+``build_gmg(mesh, K, coarse_max_dofs, smoother, n_pre, n_post)`` returns an
+``MgHierarchy`` whose levels live on the device: level 0 is the matrix-free
+stiffness operator, coarse levels are Galerkin 3^d-point block stencils
+(P^T A P computed on the GPU), the coarsest level is inverted densely once.
+``vcycle``/``apply`` run Alg. 1 (multigrid.py:231) with a zero initial guess.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._dev import as_dev, empty_dev, ptr, stream_ptr
+
+SMOOTHER_KINDS = {"weighted_jacobi": 0, "block_jacobi": 1, "chebyshev": 2}
+PROVENANCE = {0: "geometric", 1: "algebraic"}
+DEFAULT_STRENGTH_BETA = 0.003  # multigrid.py:22
+
+
+@dataclass(frozen=True)
+class SmootherConfig:
+    """multigrid.py:30; kind 'chebyshev' is the Jacobi-preconditioned Chebyshev
+    extension (degree = inner_iterations, Lanczos bound over lanczos_steps)."""
+
+    kind: str = "weighted_jacobi"
+    weight: float = 0.5
+    inner_iterations: int = 2
+    block_size: int = 2
+    lanczos_steps: int = 10
+    seed: int = 0
+
+    def __post_init__(self):
+        if not (0 < self.weight <= 1):
+            raise ValueError("smoother weight must be in (0, 1]")
+        if self.inner_iterations < 1:
+            raise ValueError("inner_iterations must be >= 1")
+
+    @property
+    def stationary(self):
+        return self.kind in ("weighted_jacobi", "block_jacobi")
+
+    def desc(self):
+        if self.kind not in SMOOTHER_KINDS:
+            raise ValueError("unknown smoother kind %r" % self.kind)
+        d = _lib.SmootherDesc()
+        d.kind = SMOOTHER_KINDS[self.kind]
+        d.weight = float(self.weight)
+        d.inner_iterations = int(self.inner_iterations)
+        d.lanczos_steps = int(self.lanczos_steps)
+        d.seed = int(self.seed)
+        return d
+
+
+@dataclass
+class LevelView:
+    size: int
+    nonzeros: int
+    provenance: str
+    storage: str
+
+
+class MgHierarchy:
+    """Device-resident hierarchy (multigrid.py:208)."""
+
+    _STORAGE = {0: "matrix_free", 1: "stencil", 2: "bsr", 3: "dense_inverse"}
+
+    def __init__(self, handle, K, smoother_config, n_pre, n_post, flags=()):
+        self._h = handle
+        self.K = K
+        self.smoother_config = smoother_config
+        self.n_pre = n_pre
+        self.n_post = n_post
+        self.flags = list(flags)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n_levels(self):
+        return _lib.load().tmg_hierarchy_num_levels(self._h)
+
+    @property
+    def levels(self):
+        out = []
+        for k in range(self.n_levels):
+            info = _lib.LevelInfo()
+            _lib.check(_lib.load().tmg_hierarchy_level_info(self._h, k, C.byref(info)))
+            out.append(LevelView(int(info.size), int(info.nonzeros), PROVENANCE[info.provenance],
+                                 self._STORAGE[info.storage]))
+        return out
+
+    @property
+    def n_geometric(self):
+        return sum(1 for lv in self.levels[:-1] if lv.provenance == "geometric")
+
+    @property
+    def stationary(self):
+        return self.smoother_config is None or self.smoother_config.stationary
+
+    def vcycle(self, b, k=0, out=None, stream=None):
+        if not (0 <= k < self.n_levels):
+            raise IndexError("level index out of range")
+        b = as_dev(b)
+        out = empty_dev(b.numel()) if out is None else out
+        _lib.check(_lib.load().tmg_hierarchy_vcycle(self._h, k, ptr(b), ptr(out), stream_ptr(stream)))
+        return out
+
+    def apply(self, b, out=None, stream=None):
+        return self.vcycle(b, 0, out, stream)
+
+    __call__ = apply
+
+    def level_apply(self, k, x):
+        x = as_dev(x)
+        out = empty_dev(x.numel())
+        _lib.check(_lib.load().tmg_hierarchy_level_apply(self._h, k, ptr(x), ptr(out), stream_ptr(None)))
+        return out
+
+    def level_lmax(self, k):
+        v = C.c_double()
+        _lib.check(_lib.load().tmg_hierarchy_level_lmax(self._h, k, C.byref(v), stream_ptr(None)))
+        return v.value
+
+    def summary(self):
+        return [{"size": lv.size, "nonzeros": lv.nonzeros, "provenance": lv.provenance}
+                for lv in self.levels]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.tmg_hierarchy_destroy(h)
+            self._h = None
+
+
+def _coarsen_dims(dims):
+    return tuple(max(1, -(-d // 2)) for d in dims)
+
+
+def gmg_level_dims(dims, dofs_per_node, coarse_max_dofs, max_levels=None):
+    """Planned element dims per level (multigrid.py:276; + optional level cap)."""
+    out = [tuple(dims)]
+    while True:
+        cur = out[-1]
+        if dofs_per_node * int(np.prod([d + 1 for d in cur])) <= coarse_max_dofs or all(d <= 1 for d in cur):
+            break
+        if max_levels is not None and len(out) >= max_levels:
+            break
+        out.append(_coarsen_dims(cur))
+    return out
+
+
+def build_gmg(mesh, K, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, max_levels=None, stream=None):
+    """Geometric hierarchy with Galerkin coarse operators (multigrid.py:318)."""
+    smoother = smoother or SmootherConfig()
+    if smoother.kind not in SMOOTHER_KINDS:
+        raise ValueError("unknown smoother kind %r" % smoother.kind)
+    if getattr(K, "mesh", mesh) is not mesh and K.mesh != mesh:
+        raise ValueError("K was assembled on a different mesh")
+    plan = gmg_level_dims(mesh.dims, mesh.dofs_per_node, coarse_max_dofs, max_levels)
+    flags = [] if len(plan) > 1 else ["no_coarsening_possible"]
+    if max_levels is None and mesh.dofs_per_node * int(np.prod([d + 1 for d in plan[-1]])) > coarse_max_dofs:
+        flags.append("coarse_bound_not_reached")
+    h = C.c_void_p()
+    _lib.check(_lib.load().tmg_gmg_build(K.handle, int(coarse_max_dofs), int(max_levels or 0),
+                                         C.byref(smoother.desc()), int(n_pre), int(n_post),
+                                         stream_ptr(stream), C.byref(h)))
+    return MgHierarchy(h, K, smoother, n_pre, n_post, flags)

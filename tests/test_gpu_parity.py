@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Tolerances follow BASELINE.json north_star: displacement
+relative L2 <= 1e-8, compliance relative <= 1e-10, PCG iterations within +-1;
+operator / V-cycle applications are compared at 1e-12 (fp64 summation order
+is the only difference)."""
+
+import numpy as np
+import pytest
+
+from oracle import topomg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2001_01655_b200 as T  # noqa: E402
+from paper_2001_01655_b200 import problems  # noqa: E402
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def cantilever(dims, seed, void=False, h=None):
+    mesh = T.build_mesh(dims, h)
+    g = O.make_grid(dims, h)
+    dpn = len(dims)
+    ny = dims[1]
+    if len(dims) == 2:
+        left = [g.node_id(0, j) for j in range(ny + 1)]
+    else:
+        left = [g.node_id(0, j, k) for j in range(ny + 1) for k in range(dims[2] + 1)]
+    fixed = np.array([dpn * n + c for n in left for c in range(dpn)])
+    f = np.zeros(g.n_dofs)
+    f[dpn * g.node_id(*([dims[0]] + [d // 2 for d in dims[1:]])) + 1] = -1.0
+    bc = T.BoundaryConditions(fixed, f)
+    rng = np.random.default_rng(seed)
+    rho = rng.uniform(0.05, 1.0, g.n_elems)
+    if void:
+        rho = np.where(rng.uniform(size=g.n_elems) < 0.3, 1e-3, 1.0)
+    E = O.simp_modulus(rho, 3.0, 1.0, 1e-9)
+    Kref = O.assemble_stiffness(g, bc.fixed_dofs, E)
+    K = T.assemble_stiffness(mesh, bc, E)
+    return mesh, g, bc, rho, E, K, Kref
+
+
+@pytest.mark.parametrize("dims", [(6, 4), (5, 3, 3), (4, 4, 2)])
+def test_operator_apply_and_diagonal(dims):
+    mesh, g, bc, rho, E, K, Kref = cantilever(dims, 1)
+    x = np.random.default_rng(2).standard_normal(g.n_dofs)
+    assert rel(host(K @ x), Kref @ x) <= 1e-13
+    assert rel(host(K.diagonal()), Kref.diagonal()) <= 1e-14
+
+
+def test_operator_unconstrained_rigid_modes():
+    mesh = T.build_mesh((4, 3, 2))
+    K = T.assemble_stiffness(mesh, None, np.ones(mesh.element_count))
+    B = T.rigid_body_modes(mesh)
+    for j in range(B.shape[1]):
+        assert np.max(np.abs(host(K @ B[:, j]))) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,bound,kind", [
+    ((16, 8), 60, "weighted_jacobi"), ((16, 8), 60, "block_jacobi"), ((17, 9), 40, "weighted_jacobi"),
+    ((5, 3, 3), 50, "weighted_jacobi"), ((8, 4, 4), 100, "chebyshev"), ((16, 8), 60, "chebyshev")])
+def test_gmg_levels_and_vcycle(dims, bound, kind):
+    mesh, g, bc, rho, E, K, Kref = cantilever(dims, 3)
+    w = 1.0 if kind == "chebyshev" else 0.6
+    sm = T.SmootherConfig(kind=kind, weight=w, inner_iterations=2)
+    osm = O.Smoother(kind=kind, weight=w, inner_iterations=2)
+    h = T.build_gmg(mesh, K, bound, sm, n_pre=2, n_post=2)
+    ho = O.build_gmg(g, Kref, bound, osm, 2, 2)
+    assert [lv.size for lv in h.levels] == [lv.A.shape[0] for lv in ho.levels]
+    rng = np.random.default_rng(4)
+    for k, lv in enumerate(ho.levels):
+        x = rng.standard_normal(lv.A.shape[0])
+        if k < len(ho.levels) - 1 or k == 0:
+            assert rel(host(h.level_apply(k, x)), lv.A @ x) <= 1e-12, k
+        if kind == "chebyshev" and k < len(ho.levels) - 1:
+            lm = h.level_lmax(k)
+            assert abs(lm - lv.smoother.lmax_estimate) <= 1e-10 * lv.smoother.lmax_estimate
+    b = rng.standard_normal(g.n_dofs)
+    assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-10
+    # coarse base case of Alg. 1 and level-range errors
+    kc = len(ho.levels) - 1
+    bc_ = rng.standard_normal(ho.levels[kc].A.shape[0])
+    assert rel(host(h.vcycle(bc_, kc)), ho.vcycle(bc_, kc)) <= 1e-9
+    with pytest.raises(IndexError):
+        h.vcycle(b, 99)
+
+
+def test_vcycle_zero_rhs_and_linearity():
+    mesh, g, bc, rho, E, K, Kref = cantilever((8, 4), 5)
+    h = T.build_gmg(mesh, K, 40, T.SmootherConfig(weight=0.6), 2, 2)
+    assert np.all(host(h.apply(np.zeros(g.n_dofs))) == 0.0)
+    rng = np.random.default_rng(1)
+    b1, b2 = rng.standard_normal(g.n_dofs), rng.standard_normal(g.n_dofs)
+    lhs = host(h.apply(2 * b1 - 3 * b2))
+    rhs = 2 * host(h.apply(b1)) - 3 * host(h.apply(b2))
+    assert np.linalg.norm(lhs - rhs) <= 1e-10 * np.linalg.norm(rhs)
+
+
+def test_single_level_is_direct_solve():
+    mesh, g, bc, rho, E, K, Kref = cantilever((4, 2), 6)
+    h = T.build_gmg(mesh, K, g.n_dofs + 1)
+    assert h.n_levels == 1
+    b = np.random.default_rng(0).standard_normal(g.n_dofs)
+    assert rel(host(h.apply(b)), np.linalg.solve(Kref.toarray(), b)) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,levels,kind,void", [
+    ((32, 16), 3, "weighted_jacobi", False), ((32, 16), 3, "weighted_jacobi", True),
+    ((12, 6, 6), 3, "weighted_jacobi", True), ((12, 6, 6), 3, "chebyshev", True)])
+def test_pcg_matches_oracle(dims, levels, kind, void):
+    mesh, g, bc, rho, E, K, Kref = cantilever(dims, 7, void=void)
+    w = 1.0 if kind == "chebyshev" else 0.6
+    h = T.build_gmg(mesh, K, 1, T.SmootherConfig(kind=kind, weight=w), 2, 2, max_levels=levels)
+    ho = O.build_gmg(g, Kref, 1, O.Smoother(kind=kind, weight=w), 2, 2, max_levels=levels)
+    cfg = T.SolveConfig(rtol=1e-8, max_iterations=2000)
+    u, rec = T.cg_solve(K, bc.load_vector, None, h, cfg)
+    uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=2000)
+    assert rec.converged and reco.converged
+    assert abs(rec.iterations - reco.iterations) <= 1
+    assert rel(host(u), uo) <= 1e-8
+    c, co = float(bc.load_vector @ host(u)), float(bc.load_vector @ uo)
+    assert abs(c - co) <= 1e-10 * abs(co)
+    hist = np.array(rec.residual_history)
+    n = min(len(hist), len(reco.residual_history))
+    assert np.allclose(hist[:n], reco.residual_history[:n], rtol=1e-6)
+
+
+def test_pcg_warm_start_and_unpreconditioned():
+    mesh, g, bc, rho, E, K, Kref = cantilever((10, 5), 8)
+    cfg = T.SolveConfig(rtol=1e-10, max_iterations=5000)
+    u, rec = T.cg_solve(K, bc.load_vector, None, None, cfg)
+    uo, reco = O.pcg(Kref, bc.load_vector, None, None, rtol=1e-10, max_iterations=5000)
+    assert abs(rec.iterations - reco.iterations) <= 1 and rel(host(u), uo) <= 1e-8
+    u2, rec2 = T.cg_solve(K, bc.load_vector, u, None, cfg)
+    assert rec2.iterations == 0 and rec2.converged
+
+
+def test_sensitivity_matches_oracle():
+    mesh, g, bc, rho, E, K, Kref = cantilever((6, 4), 9)
+    u = np.random.default_rng(3).standard_normal(g.n_dofs)
+    ce = host(T.element_strain_energies(mesh, u, K=K))
+    assert rel(ce, O.strain_energies(g, u)) <= 1e-13
+    mesh3, g3, *_ = cantilever((3, 2, 2), 9)
+    u3 = np.random.default_rng(4).standard_normal(g3.n_dofs)
+    assert rel(host(T.element_strain_energies(mesh3, u3)), O.strain_energies(g3, u3)) <= 1e-13
+
+
+def test_compliance_and_sensitivity_config0():
+    w = problems.config_0()
+    g = O.make_grid(w.mesh.dims)
+    law = T.SimpLaw(penalty=3.0, e_min_ratio=1e-9)
+    harness = T.SolverHarness(mesh=w.mesh, strategy="gmg", coarse_max_dofs=1,
+                              smoother=T.SmootherConfig(weight=0.6), n_pre=2, n_post=2, max_levels=3,
+                              solve_cfg=T.SolveConfig(rtol=1e-8))
+    F, dF, aux = T.compliance_and_sensitivity(w.mesh, w.bc, None, law, w.rho, harness)
+    Kref = O.assemble_stiffness(g, w.bc.fixed_dofs, w.moduli)
+    ho = O.build_gmg(g, Kref, 1, O.Smoother(weight=0.6), 2, 2, max_levels=3)
+    uo, reco = O.pcg(Kref, w.bc.load_vector, None, ho.apply, rtol=1e-8)
+    Fo, dco = O.compliance_sensitivity(g, w.bc.load_vector, uo, w.rho, 3.0, 1.0, 1e-9)
+    assert abs(aux["record"].iterations - reco.iterations) <= 1
+    assert rel(host(aux["u"]), uo) <= 1e-8
+    assert abs(F - Fo) <= 1e-10 * abs(Fo)
+    assert rel(dF, dco) <= 1e-8
+    assert np.all(dF <= 0)
+
+
+def test_error_behaviour():
+    mesh, g, bc, rho, E, K, Kref = cantilever((4, 2), 1)
+    with pytest.raises(ValueError):
+        T.assemble_stiffness(mesh, bc, -np.ones(mesh.element_count))
+    with pytest.raises(ValueError):
+        T.SmootherConfig(weight=0.0)
+    with pytest.raises(ValueError):
+        T.cg_solve(K, np.zeros(3))
