@@ -126,7 +126,7 @@ def oracle_sample(w, leg, iters):
     if leg["smoother"] == "chebyshev":
         sm = O.Smoother("chebyshev", 1.0, leg.get("degree", 2))
     else:
-        sm = O.Smoother(leg["smoother"], leg.get("weight", 0.5))
+        sm = O.Smoother(leg["smoother"], leg.get("weight", 0.5), safeguard=leg.get("safeguard", 0.0))
     h = O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
     u, rec = O.pcg(K, w.bc.load_vector, None, h.apply, rtol=w.rtol, max_iterations=iters)
     O.compliance_sensitivity(g, w.bc.load_vector, u, w.rho, problems.PENAL, problems.E0, problems.EMIN)

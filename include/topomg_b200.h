@@ -55,6 +55,8 @@ typedef struct {
   int32_t inner_iterations;
   int32_t lanczos_steps;
   uint64_t seed;
+  double safeguard;  /* weighted_jacobi only: >0 caps the weight of every level at
+                        safeguard/lambda_hat(D^-1 A) (Lanczos); 0 = reference behaviour */
 } tmg_smoother_desc;
 
 /* SolveConfig (krylov.py:17) for the preconditioned CG extension. */

@@ -24,6 +24,7 @@ configurable strength threshold for SA-AMG.
 
 from __future__ import annotations
 
+import dataclasses
 import time
 from dataclasses import dataclass, field
 
@@ -295,6 +296,7 @@ class Smoother:
     block_size: int = 2
     lanczos_steps: int = 10         # EXTENSION (chebyshev)
     seed: int = 0                   # EXTENSION (chebyshev start vector)
+    safeguard: float = 0.0          # EXTENSION: >0 caps the Jacobi weight at safeguard/lambda_hat
 
     def __post_init__(self):
         if not 0 < self.weight <= 1:
@@ -348,6 +350,12 @@ class JacobiSweeps:
         if np.any(d == 0):
             raise ValueError("zero diagonal entry; operator not smoothable")
         self.A, self.dinv, self.w = A, 1.0 / d, cfg.weight
+        self.lmax_estimate = None
+        if cfg.safeguard > 0:
+            # EXTENSION: keep w*lambda_max(D^-1 A) below `safeguard` (< 2) so the
+            # symmetric V-cycle stays SPD on Galerkin levels where it would not.
+            self.lmax_estimate = lanczos_max_eig(A, self.dinv, cfg.lanczos_steps, cfg.seed)
+            self.w = min(cfg.weight, cfg.safeguard / self.lmax_estimate)
 
     def apply(self, x, b, passes):
         for _ in range(passes):
@@ -423,8 +431,7 @@ def make_smoother(cfg, A, block_size=None):
     if cfg.kind not in SMOOTHERS:
         raise ValueError("unknown smoother kind %r" % cfg.kind)
     if block_size is not None and cfg.kind == "block_jacobi" and block_size != cfg.block_size:
-        cfg = Smoother(cfg.kind, cfg.weight, cfg.inner_iterations, block_size,
-                       cfg.lanczos_steps, cfg.seed)
+        cfg = dataclasses.replace(cfg, block_size=block_size)
     return SMOOTHERS[cfg.kind](A, cfg)
 
 

@@ -70,12 +70,10 @@ __global__ void k_check_pos(const double* __restrict__ v, long long n, unsigned*
 
 // ce_e = u_e^T KE u_e ; optional dc_e = -dE/drho ce_e  (optimization.py:106-129)
 template <int DIM>
-__global__ void __launch_bounds__(TPB) k_strain(FineOp<DIM> op, const double* __restrict__ u, long long nelem,
-                                                double* __restrict__ ce, const double* __restrict__ rho,
-                                                double p, double e0, double emin, double* __restrict__ dc) {
-  extern __shared__ double tmg_smem[];
-  op.init(tmg_smem);
-  __syncthreads();
+__global__ void __launch_bounds__(TPB) k_strain(const __grid_constant__ FineOp<DIM> op, const double* __restrict__ u,
+                                                long long nelem, double* __restrict__ ce,
+                                                const double* __restrict__ rho, double p, double e0, double emin,
+                                                double* __restrict__ dc) {
   constexpr int NN = 1 << DIM, NE = DIM * NN;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= nelem) return;
@@ -95,7 +93,7 @@ __global__ void __launch_bounds__(TPB) k_strain(FineOp<DIM> op, const double* __
   for (int i = 0; i < NE; ++i) {
     double ki = 0.0;
 #pragma unroll
-    for (int j = 0; j < NE; ++j) ki += op.ske[i * NE + j] * ue[j];
+    for (int j = 0; j < NE; ++j) ki += op.ke[i * NE + j] * ue[j];
     s += ue[i] * ki;
   }
   if (ce) ce[e] = s;
@@ -206,10 +204,10 @@ int tmg_operator_apply(tmg_operator* K, const double* x, double* y, void* stream
   const Operator& o = K->op;
   if (o.dim == 2) {
     auto f = o.fine<2>();
-    k_apply<2, FineOp<2>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, x, y); ::tmg::note_launch();
+    k_apply<2, FineOp<2>><<<node_grid<2>(o.L), node_block<2>(), 0, S(stream)>>>(f, x, y); ::tmg::note_launch();
   } else {
     auto f = o.fine<3>();
-    k_apply<3, FineOp<3>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, x, y); ::tmg::note_launch();
+    k_apply<3, FineOp<3>><<<node_grid<3>(o.L), node_block<3>(), 0, S(stream)>>>(f, x, y); ::tmg::note_launch();
   }
   TMG_CUDA(cudaGetLastError());
   ABI_END
@@ -224,10 +222,10 @@ int tmg_operator_diagonal(tmg_operator* K, double* d, void* stream) {
   bad.zero(S(stream));
   if (o.dim == 2) {
     auto f = o.fine<2>();
-    k_diag<2, FineOp<2>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
+    k_diag<2, FineOp<2>><<<node_grid<2>(o.L), node_block<2>(), 0, S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
   } else {
     auto f = o.fine<3>();
-    k_diag<3, FineOp<3>><<<grid_for(o.L.n), TPB, smem_of(f), S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
+    k_diag<3, FineOp<3>><<<node_grid<3>(o.L), node_block<3>(), 0, S(stream)>>>(f, d, nullptr, bad.get()); ::tmg::note_launch();
   }
   TMG_CUDA(cudaGetLastError());
   ABI_END
@@ -241,7 +239,10 @@ static SmootherCfg to_cfg(const tmg_smoother_desc* d) {
     c.degree = d->inner_iterations;
     c.lanczos_steps = d->lanczos_steps > 0 ? d->lanczos_steps : 10;
     c.seed = d->seed;
+    c.safeguard = d->safeguard;
   }
+  TMG_REQUIRE(c.safeguard == 0.0 || (c.kind == SM_JACOBI && c.safeguard > 0.0 && c.safeguard < 2.0),
+              "safeguard applies to weighted_jacobi only and must be in (0, 2)");
   TMG_REQUIRE(c.kind >= 0 && c.kind <= 2, "unknown smoother kind");
   TMG_REQUIRE(c.weight > 0.0 && c.weight <= 1.0, "smoother weight must be in (0, 1]");
   TMG_REQUIRE(c.degree >= 1, "inner_iterations must be >= 1");
@@ -342,12 +343,12 @@ int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, d
       for (int r = 0; r < reps + 1; ++r) {
         if (r == 1) TMG_CUDA(cudaEventRecord(a, s));
         if (H.sm.kind == SM_CHEBYSHEV)
-          k_cheb<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.r.get(), l.p.get(), l.dinv.get(),
-                                                                           l.coef.get(), 1, 0, l.x.get(), l.pt.get(),
-                                                                           l.rt.get());
+          k_cheb<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, l.r.get(), l.p.get(), l.dinv.get(), l.coef.get(), 1, 0,
+                                                               l.x.get(), l.pt.get(), l.rt.get());
         else
-          k_jacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.x.get(), l.b.get(), l.dinv.get(),
-                                                                             H.sm.weight, l.xt.get());
+          k_jacobi<DIM, decltype(o), false><<<TMG_NODE_LAUNCH(l), s>>>(o, l.x.get(), l.b.get(), l.dinv.get(),
+                                                                       l.wdev.get(), l.xt.get(),
+                                                                       Red{nullptr, nullptr, nullptr});
       }
     });
   };
@@ -388,10 +389,10 @@ static void launch_strain(const Operator& o, const double* u, double* ce, const 
                           double emin, double* dc, cudaStream_t s) {
   if (o.dim == 2) {
     auto f = o.fine<2>();
-    k_strain<2><<<grid_for(o.nelem), TPB, smem_of(f), s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
+    k_strain<2><<<grid_for(o.nelem), TPB, 0, s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
   } else {
     auto f = o.fine<3>();
-    k_strain<3><<<grid_for(o.nelem), TPB, smem_of(f), s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
+    k_strain<3><<<grid_for(o.nelem), TPB, 0, s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
   }
   TMG_CUDA(cudaGetLastError());
 }

@@ -79,12 +79,11 @@ struct DevBuf {
 
 // Node lattice of a structured level: nodes lexicographic with x fastest
 // (reference mesh.py:65 node_index).  In 2D nn[2] == 1.
+// Node ids are 32-bit (checked on the host: n * dofs_per_node < 2^31).
 struct Lat {
   int nn[3];
   long long n;
-  __host__ __device__ long long id(int i, int j, int k) const {
-    return i + (long long)nn[0] * (j + (long long)nn[1] * k);
-  }
+  __host__ __device__ int id(int i, int j, int k) const { return i + nn[0] * (j + nn[1] * k); }
   __device__ void ijk(long long node, int& i, int& j, int& k) const {
     i = (int)(node % nn[0]);
     long long t = node / nn[0];
@@ -95,6 +94,16 @@ struct Lat {
     return i >= 0 && i < nn[0] && j >= 0 && j < nn[1] && k >= 0 && k < nn[2];
   }
 };
+
+// 2D/3D launch geometry: one thread per lattice node, no index division.
+template <int DIM>
+inline dim3 node_block() { return DIM == 2 ? dim3(32, 8, 1) : dim3(32, 4, 2); }
+template <int DIM>
+inline dim3 node_grid(const Lat& L) {
+  const dim3 b = node_block<DIM>();
+  return dim3((L.nn[0] + b.x - 1) / b.x, (L.nn[1] + b.y - 1) / b.y, (L.nn[2] + b.z - 1) / b.z);
+}
+inline unsigned node_blocks(const dim3& g) { return g.x * g.y * g.z; }
 
 // Deterministic grid-wide reduction: per-block partials, the last block to
 // finish sums them in a fixed order and publishes one scalar (no atomics on the
@@ -111,16 +120,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-level sum (blockDim.x multiple of 32, <= 1024). Valid in thread 0.
+// linear thread / block ids for 1D, 2D and 3D launches
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_nthreads() { return blockDim.x * blockDim.y * blockDim.z; }
+__device__ __forceinline__ unsigned lin_bid() { return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); }
+__device__ __forceinline__ unsigned lin_nblocks() { return gridDim.x * gridDim.y * gridDim.z; }
+
+// Block-level sum (thread count multiple of 32, <= 1024). Valid in linear thread 0.
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double ws[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = lin_tid();
+  const int lane = t & 31, w = t >> 5;
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) ws[w] = v;
   __syncthreads();
-  const int nw = blockDim.x >> 5;
-  v = (threadIdx.x < nw) ? ws[threadIdx.x] : 0.0;
+  const int nw = lin_nthreads() >> 5;
+  v = (t < nw) ? ws[t] : 0.0;
   if (w == 0) v = warp_sum(v);
   return v;
 }
@@ -128,21 +144,22 @@ __device__ __forceinline__ double block_sum(double v) {
 // Every thread of every block must call this (uniform control flow).
 __device__ __forceinline__ void grid_reduce(double v, const Red& r) {
   __shared__ bool last;
+  const int t = lin_tid();
+  const unsigned nb = lin_nblocks();
   double b = block_sum(v);
-  if (threadIdx.x == 0) {
-    r.partials[blockIdx.x] = b;
+  if (t == 0) {
+    r.partials[lin_bid()] = b;
     __threadfence();
     unsigned done = atomicAdd(r.counter, 1u);
-    last = (done == gridDim.x - 1);
+    last = (done == nb - 1);
   }
   __syncthreads();
   if (last) {
     __threadfence();
     double s = 0.0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
-      s += ((volatile double*)r.partials)[i];
+    for (unsigned i = t; i < nb; i += lin_nthreads()) s += ((volatile double*)r.partials)[i];
     s = block_sum(s);
-    if (threadIdx.x == 0) {
+    if (t == 0) {
       *r.result = s;
       *r.counter = 0u;
     }

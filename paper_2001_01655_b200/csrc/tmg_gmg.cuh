@@ -2,10 +2,19 @@
 // level 0 is the matrix-free FineOp, coarser levels are Galerkin stencils built by
 // k_rap, the coarsest is inverted densely.  The V-cycle (multigrid.py:231) is an
 // enqueue-only host routine, so it can be captured into a CUDA graph.
+//
+// Kernel fusion in the weighted-Jacobi V-cycle (same arithmetic as Alg. 1):
+//   * the zero-start first pre-sweep x = w D^-1 b of a coarse level is written by
+//     the restriction kernel that produces b (k_restrict), and for level 0 by the
+//     PCG update kernel that produces r;
+//   * the coarse-grid correction x += P e is evaluated on the fly inside the first
+//     post-smoothing sweep (k_prolong_jacobi);
+//   * the last level-0 sweep also reduces r.z for PCG.
 #pragma once
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstring>
 #include <memory>
 
 #include "tmg_dense.cuh"
@@ -22,6 +31,7 @@ struct SmootherCfg {
   int degree = 2;
   int lanczos_steps = 10;
   uint64_t seed = 0;
+  double safeguard = 0.0;  // >0: Jacobi weight capped at safeguard / lambda_hat (Lanczos)
 };
 
 // ----------------------------------------------------------------------------
@@ -33,16 +43,17 @@ __global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b
     s += a[i] * b[i];
   grid_reduce(s, red);
 }
-__global__ void k_scale_vec(const double* __restrict__ b, const double* __restrict__ d, double w,
+__global__ void k_scale_vec(const double* __restrict__ b, const double* __restrict__ d, const double* __restrict__ wp,
                             double* __restrict__ x, long long n) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) x[i] = w * (d[i] * b[i]);
+  if (i < n) x[i] = *wp * (d[i] * b[i]);
 }
 template <int DIM>
-__global__ void k_bscale_vec(const double* __restrict__ b, const double* __restrict__ binv, double w,
+__global__ void k_bscale_vec(const double* __restrict__ b, const double* __restrict__ binv, const double* __restrict__ wp,
                              double* __restrict__ x, long long nnodes) {
   const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (node >= nnodes) return;
+  const double w = *wp;
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     double s = 0.0;
@@ -90,8 +101,10 @@ __global__ void k_lz_next(double* __restrict__ v, double* __restrict__ vp, const
 }
 // Largest eigenvalue of the Lanczos tridiagonal by Sturm bisection, then the
 // Chebyshev step coefficients on [0.1, 1.1] * lambda (multigrid.py:129-149).
+// With wout: the safeguarded Jacobi weight min(w0, sg / lambda) instead.
 __global__ void k_lz_finish(const double* __restrict__ alpha, const double* __restrict__ beta2, int steps,
-                            int degree, double* __restrict__ coef, double* __restrict__ lmax_out) {
+                            int degree, double* __restrict__ coef, double* __restrict__ lmax_out, double w0,
+                            double sg, double* __restrict__ wout) {
   int m = steps;
   for (int j = 0; j < steps; ++j)
     if (!(sqrt(beta2[j]) > 1e-300)) { m = j + 1; break; }
@@ -116,6 +129,8 @@ __global__ void k_lz_finish(const double* __restrict__ alpha, const double* __re
   }
   const double lam = hi;
   *lmax_out = lam;
+  if (wout) *wout = fmin(w0, sg / lam);
+  if (!coef) return;
   const double a = 0.1 * lam, b = 1.1 * lam, theta = 0.5 * (b + a), delta = 0.5 * (b - a);
   double al = 0.0, be = 0.0;
   for (int i = 0; i < degree; ++i) {
@@ -146,8 +161,7 @@ struct Operator {
     for (int d = 0; d < 3; ++d) o.ne[d] = ne[d];
     o.E = E.get();
     o.mask = mask.get();
-    o.ke_g = ke.get();
-    o.ske = nullptr;
+    std::memcpy(o.ke, ke_host.data(), sizeof(o.ke));
     return o;
   }
 };
@@ -165,6 +179,7 @@ struct Level {
   DevBuf<double> b, x, xt, r, rt, p, pt;
   Coarsening T{};  // to the next level
   DevBuf<double> coef, lmax;  // Chebyshev
+  DevBuf<double> wdev;        // Jacobi weight used by the kernels (safeguarded)
 };
 
 struct Hierarchy {
@@ -176,6 +191,13 @@ struct Hierarchy {
   std::vector<int> provenance;
   RedSlot red;  // scratch reduction for setup
   int last() const { return (int)lv.size() - 1; }
+  // fused-kernel V-cycle applies (point Jacobi, at least one pre-sweep)
+  bool fused() const { return sm.kind == SM_JACOBI && n_pre > 0; }
+  // buffer receiving the first Jacobi write of level k when its output is xout
+  double* first_dst(int k, double* xout) const {
+    const int W = n_pre + n_post;
+    return ((W - 1) % 2 == 0) ? xout : lv[k]->xt.get();
+  }
 };
 
 template <int DIM, class F>
@@ -190,48 +212,57 @@ void with_op(const Level& l, F&& f) {
   }
 }
 
-template <class Op>
-inline size_t smem_of(const Op&) { return Op::SMEM * sizeof(double); }
+#define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), 0
 
 template <int DIM>
 void level_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
   with_op<DIM>(l, [&](auto o) {
-    k_apply<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, x, y); ::tmg::note_launch();
+    k_apply<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, x, y);
+    note_launch();
   });
 }
 
-// Lanczos bound + Chebyshev coefficients for a level (device only)
+// Lanczos bound + Chebyshev coefficients (or the safeguarded Jacobi weight) for
+// a level, device only.
 template <int DIM>
-void chebyshev_setup(Hierarchy& H, Level& l, cudaStream_t s) {
+void lanczos_setup(Hierarchy& H, Level& l, cudaStream_t s) {
   const int m = H.sm.lanczos_steps;
   DevBuf<double> v, vp, w, alpha, beta2, nrm;
   v.alloc(l.ndof, s); vp.alloc(l.ndof, s); w.alloc(l.ndof, s);
   alpha.alloc(std::max(m, 1), s); beta2.alloc(std::max(m, 1), s); nrm.alloc(1, s);
   alpha.zero(s); beta2.zero(s);
-  l.coef.alloc(2 * std::max(H.sm.degree, 1), s);
+  const bool cheb = H.sm.kind == SM_CHEBYSHEV;
+  if (cheb) l.coef.alloc(2 * std::max(H.sm.degree, 1), s);
   l.lmax.alloc(1, s);
   const unsigned g = grid_for(l.ndof);
   const unsigned gr = std::min<unsigned>(g, 1184);
-  k_splitmix<<<g, TPB, 0, s>>>(v.get(), l.ndof, (unsigned long long)H.sm.seed); ::tmg::note_launch();
+  k_splitmix<<<g, TPB, 0, s>>>(v.get(), l.ndof, (unsigned long long)H.sm.seed);
   Red rn = H.red.red();
   rn.result = nrm.get();
-  k_dot<<<gr, TPB, 0, s>>>(v.get(), v.get(), l.ndof, rn); ::tmg::note_launch();
-  k_div_sqrt<<<g, TPB, 0, s>>>(v.get(), nrm.get(), l.ndof); ::tmg::note_launch();
+  k_dot<<<gr, TPB, 0, s>>>(v.get(), v.get(), l.ndof, rn);
+  k_div_sqrt<<<g, TPB, 0, s>>>(v.get(), nrm.get(), l.ndof);
+  note_launch(3);
   for (int j = 0; j < m; ++j) {
     with_op<DIM>(l, [&](auto o) {
-      k_apply_sym<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, v.get(), l.dsq.get(), w.get()); ::tmg::note_launch();
+      k_apply_sym<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, v.get(), l.dsq.get(), w.get());
     });
     Red ra = H.red.red();
     ra.result = alpha.get() + j;
-    k_dot<<<gr, TPB, 0, s>>>(w.get(), v.get(), l.ndof, ra); ::tmg::note_launch();
+    k_dot<<<gr, TPB, 0, s>>>(w.get(), v.get(), l.ndof, ra);
     k_lz_orth<<<g, TPB, 0, s>>>(w.get(), v.get(), vp.get(), alpha.get() + j, j > 0 ? beta2.get() + j - 1 : nullptr,
-                                l.ndof); ::tmg::note_launch();
+                                l.ndof);
     Red rb = H.red.red();
     rb.result = beta2.get() + j;
-    k_dot<<<gr, TPB, 0, s>>>(w.get(), w.get(), l.ndof, rb); ::tmg::note_launch();
-    if (j + 1 < m) { k_lz_next<<<g, TPB, 0, s>>>(v.get(), vp.get(), w.get(), beta2.get() + j, l.ndof); ::tmg::note_launch(); }
+    k_dot<<<gr, TPB, 0, s>>>(w.get(), w.get(), l.ndof, rb);
+    note_launch(4);
+    if (j + 1 < m) {
+      k_lz_next<<<g, TPB, 0, s>>>(v.get(), vp.get(), w.get(), beta2.get() + j, l.ndof);
+      note_launch();
+    }
   }
-  k_lz_finish<<<1, 1, 0, s>>>(alpha.get(), beta2.get(), m, H.sm.degree, l.coef.get(), l.lmax.get()); ::tmg::note_launch();
+  k_lz_finish<<<1, 1, 0, s>>>(alpha.get(), beta2.get(), m, H.sm.degree, cheb ? l.coef.get() : nullptr, l.lmax.get(),
+                              H.sm.weight, H.sm.safeguard, cheb ? nullptr : l.wdev.get());
+  note_launch();
   TMG_CUDA(cudaGetLastError());
 }
 
@@ -241,15 +272,19 @@ void level_setup(Hierarchy& H, Level& l, bool smoother_needed, cudaStream_t s, D
   l.diag.alloc(nd, s);
   l.dinv.alloc(nd, s);
   const bool cheb = H.sm.kind == SM_CHEBYSHEV;
-  if (cheb) l.dsq.alloc(nd, s);
+  const bool guard = H.sm.kind == SM_JACOBI && H.sm.safeguard > 0.0;
+  if (cheb || guard) l.dsq.alloc(nd, s);
   if (H.sm.kind == SM_BLOCK_JACOBI) l.binv.alloc(nd * DIM, s);
   with_op<DIM>(l, [&](auto o) {
-    k_diag<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, l.diag.get(), l.binv.get(), bad.get()); ::tmg::note_launch();
+    k_diag<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, l.diag.get(), l.binv.get(), bad.get());
   });
-  k_recip<<<grid_for(nd), TPB, 0, s>>>(l.diag.get(), l.dinv.get(), cheb ? l.dsq.get() : nullptr, nd); ::tmg::note_launch();
+  k_recip<<<grid_for(nd), TPB, 0, s>>>(l.diag.get(), l.dinv.get(), (cheb || guard) ? l.dsq.get() : nullptr, nd);
+  note_launch(2);
+  l.wdev.alloc(1, s);
+  TMG_CUDA(cudaMemcpyAsync(l.wdev.get(), &H.sm.weight, sizeof(double), cudaMemcpyHostToDevice, s));
   l.b.alloc(nd, s); l.x.alloc(nd, s); l.xt.alloc(nd, s); l.r.alloc(nd, s);
   if (cheb) { l.rt.alloc(nd, s); l.p.alloc(nd, s); l.pt.alloc(nd, s); }
-  if (cheb && smoother_needed) chebyshev_setup<DIM>(H, l, s);
+  if ((cheb || guard) && smoother_needed) lanczos_setup<DIM>(H, l, s);
 }
 
 inline int coarsen1(int d) { return std::max(1, (d + 1) / 2); }
@@ -305,7 +340,8 @@ std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dof
       l->A.alloc((size_t)Slots<DIM>::NS * DIM * DIM * l->L.n, s);
       with_op<DIM>(f, [&](auto o) {
         const long long nt = l->L.n * Slots<DIM>::NS;
-        k_rap<DIM, decltype(o)><<<grid_for(nt), TPB, smem_of(o), s>>>(o, T, l->A.get()); ::tmg::note_launch();
+        k_rap<DIM, decltype(o)><<<grid_for(nt), TPB, 0, s>>>(o, T, l->A.get());
+        note_launch();
       });
       TMG_CUDA(cudaGetLastError());
     }
@@ -319,7 +355,8 @@ std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dof
   H->coarse.A.alloc((size_t)c.ndof * c.ndof, s);
   H->coarse.A.zero(s);
   with_op<DIM>(c, [&](auto o) {
-    k_to_dense<DIM, decltype(o)><<<grid_for(c.L.n), TPB, smem_of(o), s>>>(o, H->coarse.A.get()); ::tmg::note_launch();
+    k_to_dense<DIM, decltype(o)><<<TMG_NODE_LAUNCH(c), s>>>(o, H->coarse.A.get());
+    note_launch();
   });
   H->coarse.build(s);
   unsigned hbad = 0, cbad = 0;
@@ -335,30 +372,6 @@ std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dof
 // ----------------------------------------------------------------------------
 // V-cycle (multigrid.py:231), enqueue only
 // ----------------------------------------------------------------------------
-template <int DIM>
-void smooth_jacobi(Hierarchy& H, Level& l, const double* b, double*& cur, int passes, double* const bufs[2],
-                   int& widx, int W, cudaStream_t s) {
-  for (int p = 0; p < passes; ++p) {
-    ++widx;
-    double* dst = ((W - widx) % 2 == 0) ? bufs[0] : bufs[1];
-    if (cur == nullptr) {  // zero start: x = w D^-1 b without a product
-      if (H.sm.kind == SM_BLOCK_JACOBI)
-        k_bscale_vec<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(b, l.binv.get(), H.sm.weight, dst, l.L.n);
-      else
-        k_scale_vec<<<grid_for(l.ndof), TPB, 0, s>>>(b, l.dinv.get(), H.sm.weight, dst, l.ndof);
-      ::tmg::note_launch();
-    } else {
-      with_op<DIM>(l, [&](auto o) {
-        if (H.sm.kind == SM_BLOCK_JACOBI)
-          k_bjacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, cur, b, l.binv.get(), H.sm.weight, dst);
-        else
-          k_jacobi<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, cur, b, l.dinv.get(), H.sm.weight, dst);
-        ::tmg::note_launch();
-      });
-    }
-    cur = dst;
-  }
-}
 
 // Chebyshev passes on x (in place); x_zero: x holds garbage and means 0.
 template <int DIM>
@@ -368,9 +381,8 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
     if (x_zero) {
       rin = b;
     } else {
-      with_op<DIM>(l, [&](auto o) {
-        k_residual<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, x, b, l.r.get()); ::tmg::note_launch();
-      });
+      with_op<DIM>(l, [&](auto o) { k_residual<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, x, b, l.r.get()); });
+      note_launch();
       rin = l.r.get();
     }
     const double* pin = l.p.get();
@@ -382,9 +394,10 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
       if (ro == rin) ro = rbuf[(i + 1) % 2];
       if (po == pin) po = pbuf[(i + 1) % 2];
       with_op<DIM>(l, [&](auto o) {
-        k_cheb<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, rin, pin, l.dinv.get(), l.coef.get(), i,
-                                                                         (x_zero && i == 0) ? 1 : 0, x, po, ro); ::tmg::note_launch();
+        k_cheb<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, rin, pin, l.dinv.get(), l.coef.get(), i,
+                                                             (x_zero && i == 0) ? 1 : 0, x, po, ro);
       });
+      note_launch();
       rin = ro;
       pin = po;
     }
@@ -392,46 +405,117 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
   }
 }
 
+// One Jacobi (point or block) sweep cur -> dst; cur == nullptr means x = 0.
+template <int DIM, bool DOT>
+void jacobi_sweep(Hierarchy& H, Level& l, const double* b, const double* cur, double* dst, const Red& red,
+                  cudaStream_t s) {
+  if (cur == nullptr) {
+    if (H.sm.kind == SM_BLOCK_JACOBI)
+      k_bscale_vec<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(b, l.binv.get(), l.wdev.get(), dst, l.L.n);
+    else
+      k_scale_vec<<<grid_for(l.ndof), TPB, 0, s>>>(b, l.dinv.get(), l.wdev.get(), dst, l.ndof);
+  } else {
+    with_op<DIM>(l, [&](auto o) {
+      if (H.sm.kind == SM_BLOCK_JACOBI)
+        k_bjacobi<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, cur, b, l.binv.get(), l.wdev.get(), dst);
+      else
+        k_jacobi<DIM, decltype(o), DOT><<<TMG_NODE_LAUNCH(l), s>>>(o, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
+    });
+  }
+  note_launch();
+}
+
+// V-cycle on level k: xout = MG(b).  first_done: the first pre-sweep result
+// w D^-1 b already sits in H.first_dst(k, xout).  dot (level 0 only): reduce
+// xout . b in the last post-sweep.  Returns true if dot was produced.
 template <int DIM>
-void vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s) {
+bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, bool first_done = false,
+            const Red* dot = nullptr) {
   Level& l = *H.lv[k];
   if (k == H.last()) {
     H.coarse.apply(b, xout, s);
-    return;
+    return false;
   }
   Level& c = *H.lv[k + 1];
+  const bool cheb = H.sm.kind == SM_CHEBYSHEV;
+  const int W = H.n_pre + H.n_post;
+  auto buf = [&](int w) { return ((W - w) % 2 == 0) ? xout : l.xt.get(); };
+  const Red nored{nullptr, nullptr, nullptr};
   double* xcur = nullptr;
-  if (H.sm.kind == SM_CHEBYSHEV) {
-    if (H.n_pre > 0) { smooth_cheb<DIM>(H, l, b, xout, true, H.n_pre, s); xcur = xout; }
+  int widx = 0;
+  if (cheb) {
+    if (H.n_pre > 0) {
+      smooth_cheb<DIM>(H, l, b, xout, true, H.n_pre, s);
+      xcur = xout;
+    }
   } else {
-    double* const bufs[2] = {xout, l.xt.get()};
-    int widx = 0;
-    const int W = H.n_pre + H.n_post;
-    smooth_jacobi<DIM>(H, l, b, xcur, H.n_pre, bufs, widx, W, s);
+    for (int p = 0; p < H.n_pre; ++p) {
+      double* dst = buf(++widx);
+      if (!(p == 0 && first_done)) jacobi_sweep<DIM, false>(H, l, b, xcur, dst, nored, s);
+      xcur = dst;
+    }
   }
   const double* r = b;
   if (xcur) {
-    with_op<DIM>(l, [&](auto o) {
-      k_residual<DIM, decltype(o)><<<grid_for(l.L.n), TPB, smem_of(o), s>>>(o, xcur, b, l.r.get()); ::tmg::note_launch();
-    });
+    with_op<DIM>(l, [&](auto o) { k_residual<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, xcur, b, l.r.get()); });
+    note_launch();
     r = l.r.get();
   }
-  k_restrict<DIM><<<grid_for(c.L.n), TPB, 0, s>>>(l.T, r, c.b.get(), nullptr, 0.0, nullptr); ::tmg::note_launch();
-  vcycle<DIM>(H, k + 1, c.b.get(), c.x.get(), s);
-  if (!xcur) {
-    xcur = (H.sm.kind == SM_CHEBYSHEV || H.n_post % 2 == 0) ? xout : l.xt.get();
-    TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
-  }
-  k_prolong_add<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(l.T, c.x.get(), xcur); ::tmg::note_launch();
-  if (H.sm.kind == SM_CHEBYSHEV) {
-    smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);
+  const bool cfirst = H.fused() && k + 1 < H.last();
+  double* cx_first = cfirst ? H.first_dst(k + 1, c.x.get()) : nullptr;
+  k_restrict<DIM><<<node_grid<DIM>(c.L), node_block<DIM>(), 0, s>>>(l.T, r, c.b.get(), c.dinv.get(), c.wdev.get(),
+                                                                     cx_first);
+  note_launch();
+  vcycle<DIM>(H, k + 1, c.b.get(), c.x.get(), s, cfirst, nullptr);
+  bool dot_done = false;
+  if (!cheb && H.sm.kind == SM_JACOBI && H.n_post > 0) {
+    if (!xcur) {  // no pre-smoothing: x = 0 before the correction
+      xcur = (buf(1) == xout) ? l.xt.get() : xout;
+      TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
+    }
+    for (int p = 0; p < H.n_post; ++p) {
+      double* dst = buf(++widx);
+      const bool last = p == H.n_post - 1 && dot != nullptr;
+      with_op<DIM>(l, [&](auto o) {
+        if (p == 0) {
+          if (last)
+            k_prolong_jacobi<DIM, decltype(o), true><<<TMG_NODE_LAUNCH(l), s>>>(
+                o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, *dot);
+          else
+            k_prolong_jacobi<DIM, decltype(o), false><<<TMG_NODE_LAUNCH(l), s>>>(
+                o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, nored);
+        } else {
+          if (last)
+            k_jacobi<DIM, decltype(o), true><<<TMG_NODE_LAUNCH(l), s>>>(o, xcur, b, l.dinv.get(), l.wdev.get(), dst,
+                                                                        *dot);
+          else
+            k_jacobi<DIM, decltype(o), false><<<TMG_NODE_LAUNCH(l), s>>>(o, xcur, b, l.dinv.get(), l.wdev.get(), dst,
+                                                                         nored);
+        }
+      });
+      note_launch();
+      xcur = dst;
+    }
+    dot_done = dot != nullptr;
   } else {
-    double* const bufs[2] = {xout, l.xt.get()};
-    int widx = H.n_pre;
-    const int W = H.n_pre + H.n_post;
-    smooth_jacobi<DIM>(H, l, b, xcur, H.n_post, bufs, widx, W, s);
+    if (!xcur) {
+      xcur = (cheb || H.n_post % 2 == 0) ? xout : l.xt.get();
+      TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
+    }
+    k_prolong_add<DIM><<<TMG_NODE_LAUNCH(l), s>>>(l.T, c.x.get(), xcur);
+    note_launch();
+    if (cheb) {
+      smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);
+    } else {
+      for (int p = 0; p < H.n_post; ++p) {
+        double* dst = buf(++widx);
+        jacobi_sweep<DIM, false>(H, l, b, xcur, dst, nored, s);
+        xcur = dst;
+      }
+    }
   }
   if (xcur != xout) TMG_CUDA(cudaMemcpyAsync(xout, xcur, l.ndof * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return dot_done;
 }
 
 }  // namespace tmg

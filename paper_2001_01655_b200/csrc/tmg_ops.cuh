@@ -2,19 +2,23 @@
 // apply them.  Two operator kinds share one interface:
 //
 //  * FineOp<DIM>:   the level-0 stiffness K(rho) kept matrix-free -- element moduli
-//    (8 B/element) and the unit-modulus element matrix KE staged in shared memory.
-//    A row of K is gathered node-centrically from the 2^DIM elements around the
-//    node, so the product is assembled atomic-free with no colouring pass.  The
-//    symmetric Dirichlet elimination of mesh.py:313 (Z K Z + I_fixed) is applied
-//    on the fly from a per-node free-dof bitmask.
+//    (8 B/element) and the unit-modulus element matrix KE.  KE travels BY VALUE in
+//    the kernel parameters, so every KE coefficient is a constant-bank operand of
+//    the DFMA (no shared-memory or L1 traffic for it).  A row of K is gathered
+//    node-centrically from the 2^DIM elements around the node, so the product is
+//    assembled atomic-free with no colouring pass.  The symmetric Dirichlet
+//    elimination of mesh.py:313 (Z K Z + I_fixed) is applied on the fly from a
+//    per-node free-dof bitmask.
 //  * StencilOp<DIM>: a Galerkin coarse operator P^T A P of a geometric level.  On a
 //    structured grid with bilinear/trilinear P it is exactly a 3^DIM-point nodal
 //    stencil of DIM x DIM blocks, stored structure-of-arrays
 //    A[(slot*DIM*DIM + a*DIM + b) * n_nodes + node] so that a warp reads 32
-//    consecutive doubles per (slot, a, b).  No index arrays are stored.
+//    consecutive doubles per (slot, a, b).  Out-of-domain slots hold zeros, so all
+//    coefficient loads are unconditional (full memory-level parallelism).  No index
+//    arrays are stored.
 //
-// Every kernel maps one thread to one node (x fastest), so vector loads are
-// coalesced along x and neighbour gathers hit the same cache lines.
+// Node kernels use a 2D/3D launch (32x8 / 32x4x2 threads): one thread per node,
+// x fastest, coordinates straight from blockIdx/threadIdx (no index division).
 #pragma once
 #include "tmg_common.cuh"
 
@@ -37,20 +41,95 @@ struct Slots {  // 3^DIM stencil neighbourhood, slot = (dx+1) + 3(dy+1) + 9(dz+1
   }
 };
 
+template <int DIM>
+__device__ __forceinline__ void load_node(const double* __restrict__ v, int node, double out[DIM]) {
+  if (DIM == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(v) + node);
+    out[0] = t.x;
+    out[1] = t.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = __ldg(v + node * DIM + c);
+  }
+}
+template <int DIM>
+__device__ __forceinline__ void store_node(double* __restrict__ v, int node, const double in[DIM]) {
+  if (DIM == 2) {
+    reinterpret_cast<double2*>(v)[node] = make_double2(in[0], in[1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) v[node * DIM + c] = in[c];
+  }
+}
+
 // ----------------------------------------------------------------------------
-// vector sources (functors giving the value of the vector being multiplied)
+// geometric transfers (multigrid.py:288-315): 1D hat interpolation per axis,
+// Kronecker product with x fastest, identity on axes with one element.
+// ----------------------------------------------------------------------------
+struct Coarsening {
+  Lat F, C;  // fine / coarse node lattices
+  int co[3]; // 1 if the axis is coarsened (fine element count > 1)
+};
+
+// fine candidates of coarse index I on one axis: up to 3 (index, weight)
+__device__ __forceinline__ int fine_of_coarse(int I, int co, int nf, int idx[3], double w[3]) {
+  if (!co) { idx[0] = I; w[0] = 1.0; return 1; }
+  int c = 0;
+  const int base = 2 * I;
+  if (base - 1 >= 0 && base - 1 < nf) { idx[c] = base - 1; w[c] = 0.5; ++c; }
+  if (base < nf) { idx[c] = base; w[c] = 1.0; ++c; }
+  if (base + 1 < nf) { idx[c] = base + 1; w[c] = 0.5; ++c; }
+  return c;
+}
+// coarse parents of fine index i on one axis: up to 2 (index, weight)
+__device__ __forceinline__ int coarse_of_fine(int i, int co, int idx[2], double w[2]) {
+  if (!co) { idx[0] = i; w[0] = 1.0; return 1; }
+  if ((i & 1) == 0) { idx[0] = i >> 1; w[0] = 1.0; return 1; }
+  idx[0] = (i - 1) >> 1; idx[1] = (i + 1) >> 1; w[0] = w[1] = 0.5;
+  return 2;
+}
+// (P e)(fine node i,j,k), branch-light: parents clamp to the same node with weight 0.
+template <int DIM>
+__device__ __forceinline__ void prolong_at(const Coarsening& T, const double* __restrict__ e, int i, int j, int k,
+                                           double out[DIM]) {
+  int ix[2], iy[2], iz[2];
+  double wx[2], wy[2], wz[2];
+  const int nx = coarse_of_fine(i, T.co[0], ix, wx);
+  const int ny = coarse_of_fine(j, T.co[1], iy, wy);
+  int nz = 1;
+  if (DIM == 3) nz = coarse_of_fine(k, T.co[2], iz, wz);
+  else { iz[0] = 0; wz[0] = 1.0; }
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) out[c] = 0.0;
+  for (int c2 = 0; c2 < nz; ++c2)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) {
+        const double ww = wx[a] * wy[b] * wz[c2];
+        double v[DIM];
+        load_node<DIM>(e, T.C.id(ix[a], iy[b], iz[c2]), v);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) out[c] += ww * v[c];
+      }
+}
+
+// ----------------------------------------------------------------------------
+// vector sources: value of the vector being multiplied at (node, i, j, k)
 // ----------------------------------------------------------------------------
 template <int DIM>
 struct VecSrc {
   const double* __restrict__ v;
-  __device__ double operator()(long long node, int c) const { return v[node * DIM + c]; }
+  __device__ void load(int node, int, int, int, double out[DIM]) const { load_node<DIM>(v, node, out); }
 };
 template <int DIM>
 struct ScaledSrc {  // s .* v
   const double* __restrict__ v;
   const double* __restrict__ s;
-  __device__ double operator()(long long node, int c) const {
-    return v[node * DIM + c] * s[node * DIM + c];
+  __device__ void load(int node, int, int, int, double out[DIM]) const {
+    double a[DIM], b[DIM];
+    load_node<DIM>(v, node, a);
+    load_node<DIM>(s, node, b);
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = a[c] * b[c];
   }
 };
 template <int DIM>
@@ -58,9 +137,14 @@ struct AxpySrc {  // z + beta * p  (beta == 0 -> z; never touches p then)
   const double* __restrict__ z;
   const double* __restrict__ p;
   double beta;
-  __device__ double operator()(long long node, int c) const {
-    const long long i = node * DIM + c;
-    return beta == 0.0 ? z[i] : z[i] + beta * p[i];
+  __device__ void load(int node, int, int, int, double out[DIM]) const {
+    load_node<DIM>(z, node, out);
+    if (beta != 0.0) {
+      double q[DIM];
+      load_node<DIM>(p, node, q);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] += beta * q[c];
+    }
   }
 };
 template <int DIM>
@@ -69,10 +153,31 @@ struct ChebSrc {  // dinv .* r + beta * p
   const double* __restrict__ p;
   const double* __restrict__ dinv;
   double beta;
-  __device__ double operator()(long long node, int c) const {
-    const long long i = node * DIM + c;
-    const double z = dinv[i] * r[i];
-    return beta == 0.0 ? z : z + beta * p[i];
+  __device__ void load(int node, int, int, int, double out[DIM]) const {
+    double a[DIM], d[DIM];
+    load_node<DIM>(r, node, a);
+    load_node<DIM>(dinv, node, d);
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = d[c] * a[c];
+    if (beta != 0.0) {
+      double q[DIM];
+      load_node<DIM>(p, node, q);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] += beta * q[c];
+    }
+  }
+};
+template <int DIM>
+struct ProlongSrc {  // x + P e (coarse-grid correction evaluated on the fly)
+  const double* __restrict__ x;
+  const double* __restrict__ e;
+  Coarsening T;
+  __device__ void load(int node, int i, int j, int k, double out[DIM]) const {
+    double pe[DIM];
+    load_node<DIM>(x, node, out);
+    prolong_at<DIM>(T, e, i, j, k, pe);
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] += pe[c];
   }
 };
 
@@ -82,42 +187,35 @@ struct ChebSrc {  // dinv .* r + beta * p
 template <int DIM>
 struct FineOp {
   static constexpr int NN = 1 << DIM, NE = DIM * NN, DD = DIM * DIM;
-  static constexpr int SMEM = NE * NE;  // doubles of shared memory needed
   Lat L;
   int ne[3];
   const double* __restrict__ E;
   const uint8_t* __restrict__ mask;  // bit c set -> dof c of the node is free
-  const double* __restrict__ ke_g;
-  const double* ske;
+  double ke[NE * NE];                // kernel-parameter constant bank
 
-  __device__ void init(double* smem) {
-    for (int t = threadIdx.x; t < SMEM; t += blockDim.x) smem[t] = ke_g[t];
-    ske = smem;
-  }
-  __device__ bool elem_ok(int ex, int ey, int ez) const {
-    return ex >= 0 && ex < ne[0] && ey >= 0 && ey < ne[1] && (DIM == 2 || (ez >= 0 && ez < ne[2]));
-  }
-  __device__ long long elem_id(int ex, int ey, int ez) const {
-    return ex + (long long)ne[0] * (ey + (long long)ne[1] * ez);
-  }
+  __device__ int elem_id(int ex, int ey, int ez) const { return ex + ne[0] * (ey + ne[1] * ez); }
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src
   template <class Src>
-  __device__ void row(long long node, int i, int j, int k, const Src& src, double out[DIM]) const {
+  __device__ void row(int node, int i, int j, int k, const Src& src, double out[DIM], double self[DIM]) const {
     constexpr int NS = Slots<DIM>::NS;
     double xv[NS][DIM];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
-      if (L.inside(ii, jj, kk)) {
-        const long long m = L.id(ii, jj, kk);
-        const unsigned mk = mask[m];
+      const bool in = L.inside(ii, jj, kk);
+      const int ic = min(max(ii, 0), L.nn[0] - 1), jc = min(max(jj, 0), L.nn[1] - 1);
+      const int kc = DIM == 3 ? min(max(kk, 0), L.nn[2] - 1) : 0;
+      const int m = L.id(ic, jc, kc);
+      const unsigned mk = in ? (unsigned)__ldg(mask + m) : 0u;
+      double v[DIM];
+      src.load(m, ic, jc, kc, v);
+      if (s == NS / 2) {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) xv[s][d] = ((mk >> d) & 1u) ? src(m, d) : 0.0;
-      } else {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) xv[s][d] = 0.0;
+        for (int d = 0; d < DIM; ++d) self[d] = v[d];
       }
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) xv[s][d] = ((mk >> d) & 1u) ? v[d] : 0.0;
     }
     double acc[DIM];
 #pragma unroll
@@ -129,8 +227,10 @@ struct FineOp {
 #pragma unroll
         for (int ex = 0; ex < 2; ++ex) {
           const int eI = i - 1 + ex, eJ = j - 1 + ey, eK = DIM == 3 ? k - 1 + ez : 0;
-          if (!elem_ok(eI, eJ, eK)) continue;
-          const double Ee = E[elem_id(eI, eJ, eK)];
+          const bool ok = eI >= 0 && eI < ne[0] && eJ >= 0 && eJ < ne[1] && (DIM == 2 || (eK >= 0 && eK < ne[2]));
+          const int ec = elem_id(min(max(eI, 0), ne[0] - 1), min(max(eJ, 0), ne[1] - 1),
+                                 DIM == 3 ? min(max(eK, 0), ne[2] - 1) : 0);
+          const double Ee = ok ? __ldg(E + ec) : 0.0;
           const int ln = corner_of(1 - ex, 1 - ey, DIM == 3 ? 1 - ez : 0);
           double t[DIM];
 #pragma unroll
@@ -142,14 +242,14 @@ struct FineOp {
 #pragma unroll
             for (int c = 0; c < DIM; ++c)
 #pragma unroll
-              for (int d = 0; d < DIM; ++d) t[c] += ske[(ln * DIM + c) * NE + m * DIM + d] * xv[s][d];
+              for (int d = 0; d < DIM; ++d) t[c] += ke[(ln * DIM + c) * NE + m * DIM + d] * xv[s][d];
           }
 #pragma unroll
           for (int c = 0; c < DIM; ++c) acc[c] += Ee * t[c];
         }
-    const unsigned mn = mask[node];
+    const unsigned mn = __ldg(mask + node);
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) out[c] = ((mn >> c) & 1u) ? acc[c] : src(node, c);
+    for (int c = 0; c < DIM; ++c) out[c] = ((mn >> c) & 1u) ? acc[c] : self[c];
   }
 
   // block (i -> j) of Z K Z + I_fixed, i and j lattice neighbours (|i-j|_inf <= 1)
@@ -169,7 +269,7 @@ struct FineOp {
 #pragma unroll
           for (int a = 0; a < DIM; ++a)
 #pragma unroll
-            for (int b = 0; b < DIM; ++b) blk[a * DIM + b] += Ee * ske[(li * DIM + a) * NE + lj * DIM + b];
+            for (int b = 0; b < DIM; ++b) blk[a * DIM + b] += Ee * ke[(li * DIM + a) * NE + lj * DIM + b];
         }
     const unsigned mi = mask[L.id(i0, i1, i2)], mj = mask[L.id(j0, j1, j2)];
 #pragma unroll
@@ -191,29 +291,30 @@ struct FineOp {
 template <int DIM>
 struct StencilOp {
   static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
-  static constexpr int SMEM = 0;
   Lat L;
   const double* __restrict__ A;
 
-  __device__ void init(double*) {}
-
   template <class Src>
-  __device__ void row(long long node, int i, int j, int k, const Src& src, double out[DIM]) const {
+  __device__ void row(int node, int i, int j, int k, const Src& src, double out[DIM], double self[DIM]) const {
+    const int n = (int)L.n;
     double acc[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
-      if (!L.inside(ii, jj, kk)) continue;
-      const long long m = L.id(ii, jj, kk);
+      const int ii = min(max(i + Slots<DIM>::dx(s), 0), L.nn[0] - 1);
+      const int jj = min(max(j + Slots<DIM>::dy(s), 0), L.nn[1] - 1);
+      const int kk = DIM == 3 ? min(max(k + Slots<DIM>::dz(s), 0), L.nn[2] - 1) : 0;
       double xv[DIM];
+      src.load(L.id(ii, jj, kk), ii, jj, kk, xv);  // clamped; the slot's coefficients are 0 there
+      if (s == NS / 2) {
 #pragma unroll
-      for (int b = 0; b < DIM; ++b) xv[b] = src(m, b);
+        for (int d = 0; d < DIM; ++d) self[d] = xv[d];
+      }
 #pragma unroll
       for (int a = 0; a < DIM; ++a)
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) acc[a] += A[(s * DD + a * DIM + b) * L.n + node] * xv[b];
+        for (int b = 0; b < DIM; ++b) acc[a] += __ldg(A + (s * DD + a * DIM + b) * n + node) * xv[b];
     }
 #pragma unroll
     for (int c = 0; c < DIM; ++c) out[c] = acc[c];
@@ -221,122 +322,162 @@ struct StencilOp {
 
   __device__ void block(int i0, int i1, int i2, int j0, int j1, int j2, double blk[DD]) const {
     const int s = Slots<DIM>::of(j0 - i0, j1 - i1, DIM == 3 ? j2 - i2 : 0);
-    const long long node = L.id(i0, i1, i2);
+    const int node = L.id(i0, i1, i2);
 #pragma unroll
     for (int t = 0; t < DD; ++t) blk[t] = A[(s * DD + t) * L.n + node];
   }
 };
 
 // ----------------------------------------------------------------------------
-// generic node-parallel kernels
+// generic node-parallel kernels (2D/3D launch: node_grid / node_block)
 // ----------------------------------------------------------------------------
-#define TMG_NODE_PROLOGUE                               \
-  extern __shared__ double tmg_smem[];                  \
-  op.init(tmg_smem);                                    \
-  __syncthreads();                                      \
-  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x; \
-  const bool active = node < op.L.n;                    \
-  int ci = 0, cj = 0, ck = 0;                           \
-  if (active) op.L.ijk(node, ci, cj, ck);
+#define TMG_NODE_IDX                                                                   \
+  const int ci = blockIdx.x * blockDim.x + threadIdx.x;                                \
+  const int cj = blockIdx.y * blockDim.y + threadIdx.y;                                \
+  const int ck = blockIdx.z * blockDim.z + threadIdx.z;                                \
+  const bool active = ci < op.L.nn[0] && cj < op.L.nn[1] && ck < op.L.nn[2];           \
+  const int node = active ? op.L.id(ci, cj, ck) : 0;
 
 // y = A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_apply(Op op, const double* __restrict__ x, double* __restrict__ y) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
+                                               double* __restrict__ y) {
+  TMG_NODE_IDX
   if (!active) return;
-  double out[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
-#pragma unroll
-  for (int c = 0; c < DIM; ++c) y[node * DIM + c] = out[c];
+  double out[DIM], self[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  store_node<DIM>(y, node, out);
 }
 
 // y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_apply_sym(Op op, const double* __restrict__ v, const double* __restrict__ ds,
-                                                   double* __restrict__ y) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
+                                                   const double* __restrict__ ds, double* __restrict__ y) {
+  TMG_NODE_IDX
   if (!active) return;
-  double out[DIM];
-  op.row(node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out);
+  double out[DIM], self[DIM], d[DIM];
+  op.row(node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
+  load_node<DIM>(ds, node, d);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) y[node * DIM + c] = ds[node * DIM + c] * out[c];
+  for (int c = 0; c < DIM; ++c) out[c] *= d[c];
+  store_node<DIM>(y, node, out);
 }
 
 // r = b - A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_residual(Op op, const double* __restrict__ x, const double* __restrict__ b,
-                                                  double* __restrict__ r) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
+                                                  const double* __restrict__ b, double* __restrict__ r) {
+  TMG_NODE_IDX
   if (!active) return;
-  double out[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+  double out[DIM], self[DIM], bb[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  load_node<DIM>(b, node, bb);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) r[node * DIM + c] = b[node * DIM + c] - out[c];
+  for (int c = 0; c < DIM; ++c) out[c] = bb[c] - out[c];
+  store_node<DIM>(r, node, out);
 }
 
-// xo = x + w D^-1 (b - A x)   (weighted Jacobi, multigrid.py:57)
-template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_jacobi(Op op, const double* __restrict__ x, const double* __restrict__ b,
-                                                const double* __restrict__ dinv, double w, double* __restrict__ xo) {
-  TMG_NODE_PROLOGUE
-  if (!active) return;
-  double out[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+// xo = xs + w D^-1 (b - A xs)   (weighted Jacobi sweep, multigrid.py:57) where xs is
+// the source vector (x, or x + P e when the coarse correction is fused in).
+// DOT: also reduce sum(xo . b) into red (the PCG r.z of the last level-0 sweep).
+template <int DIM, class Op, class Src, bool DOT>
+__device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const double* __restrict__ b,
+                                            const double* __restrict__ dinv, const double* __restrict__ wp,
+                                            double* __restrict__ xo, const Red& red) {
+  TMG_NODE_IDX
+  double v = 0.0;
+  if (active) {
+    const double w = *wp;
+    double out[DIM], self[DIM], bb[DIM], d[DIM];
+    op.row(node, ci, cj, ck, src, out, self);
+    load_node<DIM>(b, node, bb);
+    load_node<DIM>(dinv, node, d);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) {
-    const long long i = node * DIM + c;
-    xo[i] = x[i] + w * (dinv[i] * (b[i] - out[c]));
+    for (int c = 0; c < DIM; ++c) {
+      out[c] = self[c] + w * (d[c] * (bb[c] - out[c]));
+      if (DOT) v += out[c] * bb[c];
+    }
+    store_node<DIM>(xo, node, out);
   }
+  if (DOT) grid_reduce(v, red);
+}
+
+template <int DIM, class Op, bool DOT>
+__global__ void __launch_bounds__(TPB) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+                                                const double* __restrict__ b, const double* __restrict__ dinv,
+                                                const double* __restrict__ wp, double* __restrict__ xo, Red red) {
+  jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
+}
+
+// first post-smoothing sweep with the coarse-grid correction fused in:
+// xs = x + P e evaluated on the fly, xo = xs + w D^-1 (b - A xs)
+template <int DIM, class Op, bool DOT>
+__global__ void __launch_bounds__(TPB) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+                                                        const double* __restrict__ e, Coarsening T,
+                                                        const double* __restrict__ b, const double* __restrict__ dinv,
+                                                        const double* __restrict__ wp, double* __restrict__ xo,
+                                                        Red red) {
+  jacobi_body<DIM, Op, ProlongSrc<DIM>, DOT>(op, ProlongSrc<DIM>{x, e, T}, b, dinv, wp, xo, red);
 }
 
 // xo = x + w B^-1 (b - A x), B the nodal diagonal blocks (multigrid.py:90)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_bjacobi(Op op, const double* __restrict__ x, const double* __restrict__ b,
-                                                 const double* __restrict__ binv, double w, double* __restrict__ xo) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+                                                 const double* __restrict__ b, const double* __restrict__ binv,
+                                                 const double* __restrict__ wp, double* __restrict__ xo) {
+  TMG_NODE_IDX
   if (!active) return;
-  double out[DIM], r[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out);
+  const double w = *wp;
+  double out[DIM], self[DIM], r[DIM];
+  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  load_node<DIM>(b, node, r);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) r[c] = b[node * DIM + c] - out[c];
+  for (int c = 0; c < DIM; ++c) r[c] -= out[c];
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < DIM; ++c) s += binv[node * DIM * DIM + a * DIM + c] * r[c];
-    xo[node * DIM + a] = x[node * DIM + a] + w * s;
+    out[a] = self[a] + w * s;
   }
+  store_node<DIM>(xo, node, out);
 }
 
 // One Chebyshev step (multigrid.py:131 recurrence, SOR solve -> D^-1):
 //   p' = D^-1 r + beta p ; x += alpha p' ; r' = r - alpha A p'
-// alpha/beta of step `step` come from the device coefficient array.
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_cheb(Op op, const double* __restrict__ r, const double* __restrict__ p,
-                                              const double* __restrict__ dinv, const double* __restrict__ coef,
-                                              int step, int x_zero, double* __restrict__ x,
-                                              double* __restrict__ po, double* __restrict__ ro) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
+                                              const double* __restrict__ p, const double* __restrict__ dinv,
+                                              const double* __restrict__ coef, int step, int x_zero,
+                                              double* __restrict__ x, double* __restrict__ po,
+                                              double* __restrict__ ro) {
+  TMG_NODE_IDX
   if (!active) return;
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
-  ChebSrc<DIM> src{r, p, dinv, beta};
-  double out[DIM];
-  op.row(node, ci, cj, ck, src, out);
+  double out[DIM], pv[DIM], rr[DIM], xv[DIM];
+  op.row(node, ci, cj, ck, ChebSrc<DIM>{r, p, dinv, beta}, out, pv);
+  load_node<DIM>(r, node, rr);
+  if (x_zero) {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) xv[c] = 0.0;
+  } else {
+    load_node<DIM>(x, node, xv);
+  }
 #pragma unroll
   for (int c = 0; c < DIM; ++c) {
-    const long long i = node * DIM + c;
-    const double pv = src(node, c);
-    po[i] = pv;
-    x[i] = (x_zero ? 0.0 : x[i]) + alpha * pv;
-    ro[i] = r[i] - alpha * out[c];
+    xv[c] += alpha * pv[c];
+    rr[c] -= alpha * out[c];
   }
+  store_node<DIM>(po, node, pv);
+  store_node<DIM>(x, node, xv);
+  store_node<DIM>(ro, node, rr);
 }
 
 // diagonal / nodal block inverses of a level operator
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_diag(Op op, double* __restrict__ diag, double* __restrict__ binv,
-                                              unsigned* __restrict__ bad) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_diag(const __grid_constant__ Op op, double* __restrict__ diag,
+                                              double* __restrict__ binv, unsigned* __restrict__ bad) {
+  TMG_NODE_IDX
   if (!active) return;
   double blk[DIM * DIM];
   op.block(ci, cj, ck, ci, cj, ck, blk);
@@ -367,8 +508,8 @@ __global__ void __launch_bounds__(TPB) k_diag(Op op, double* __restrict__ diag, 
 
 // dense row-major copy of a level operator (small coarsest levels only)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_to_dense(Op op, double* __restrict__ Ad) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_to_dense(const __grid_constant__ Op op, double* __restrict__ Ad) {
+  TMG_NODE_IDX
   if (!active) return;
   const long long n = op.L.n * DIM;
   for (int s = 0; s < Slots<DIM>::NS; ++s) {
@@ -378,52 +519,28 @@ __global__ void __launch_bounds__(TPB) k_to_dense(Op op, double* __restrict__ Ad
     op.block(ci, cj, ck, ii, jj, kk, blk);
     const long long m = op.L.id(ii, jj, kk);
     for (int a = 0; a < DIM; ++a)
-      for (int b = 0; b < DIM; ++b) Ad[(node * DIM + a) * n + m * DIM + b] = blk[a * DIM + b];
+      for (int b = 0; b < DIM; ++b) Ad[((long long)node * DIM + a) * n + m * DIM + b] = blk[a * DIM + b];
   }
 }
 
-// ----------------------------------------------------------------------------
-// geometric transfers (multigrid.py:288-315): 1D hat interpolation per axis,
-// Kronecker product with x fastest, identity on axes with one element.
-// ----------------------------------------------------------------------------
-struct Coarsening {
-  Lat F, C;       // fine / coarse node lattices
-  int co[3];      // 1 if the axis is coarsened (fine element count > 1)
-};
-
-// fine candidates of coarse index I on one axis: up to 3 (index, weight)
-__device__ __forceinline__ int fine_of_coarse(int I, int co, int nf, int idx[3], double w[3]) {
-  if (!co) { idx[0] = I; w[0] = 1.0; return 1; }
-  int c = 0;
-  const int base = 2 * I;
-  if (base - 1 >= 0 && base - 1 < nf) { idx[c] = base - 1; w[c] = 0.5; ++c; }
-  if (base < nf) { idx[c] = base; w[c] = 1.0; ++c; }
-  if (base + 1 < nf) { idx[c] = base + 1; w[c] = 0.5; ++c; }
-  return c;
-}
-// coarse parents of fine index i on one axis: up to 2 (index, weight)
-__device__ __forceinline__ int coarse_of_fine(int i, int co, int idx[2], double w[2]) {
-  if (!co) { idx[0] = i; w[0] = 1.0; return 1; }
-  if ((i & 1) == 0) { idx[0] = i >> 1; w[0] = 1.0; return 1; }
-  idx[0] = (i - 1) >> 1; idx[1] = (i + 1) >> 1; w[0] = w[1] = 0.5;
-  return 2;
-}
-
 // bc = P^T r ; optionally the first (zero-start) Jacobi sweep of the coarse level:
-// xc = w * dinvc .* bc
+// xc = w * dinvc .* bc  (fused so the coarse level starts with one kernel fewer)
 template <int DIM>
 __global__ void __launch_bounds__(TPB) k_restrict(Coarsening T, const double* __restrict__ r, double* __restrict__ bc,
-                                                  const double* __restrict__ dinvc, double w, double* __restrict__ xc) {
-  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (node >= T.C.n) return;
-  int I, J, K;
-  T.C.ijk(node, I, J, K);
+                                                  const double* __restrict__ dinvc, const double* __restrict__ wp,
+                                                  double* __restrict__ xc) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  const int J = blockIdx.y * blockDim.y + threadIdx.y;
+  const int K = blockIdx.z * blockDim.z + threadIdx.z;
+  if (!(I < T.C.nn[0] && J < T.C.nn[1] && K < T.C.nn[2])) return;
+  const int node = T.C.id(I, J, K);
   int ix[3], iy[3], iz[3];
   double wx[3], wy[3], wz[3];
   const int nx = fine_of_coarse(I, T.co[0], T.F.nn[0], ix, wx);
   const int ny = fine_of_coarse(J, T.co[1], T.F.nn[1], iy, wy);
-  const int nz = DIM == 3 ? fine_of_coarse(K, T.co[2], T.F.nn[2], iz, wz) : 1;
-  if (DIM == 2) { iz[0] = 0; wz[0] = 1.0; }
+  int nz = 1;
+  if (DIM == 3) nz = fine_of_coarse(K, T.co[2], T.F.nn[2], iz, wz);
+  else { iz[0] = 0; wz[0] = 1.0; }
   double acc[DIM];
 #pragma unroll
   for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
@@ -431,53 +548,43 @@ __global__ void __launch_bounds__(TPB) k_restrict(Coarsening T, const double* __
     for (int b = 0; b < ny; ++b)
       for (int a = 0; a < nx; ++a) {
         const double ww = wx[a] * wy[b] * wz[c2];
-        const long long f = T.F.id(ix[a], iy[b], iz[c2]);
+        double v[DIM];
+        load_node<DIM>(r, T.F.id(ix[a], iy[b], iz[c2]), v);
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) acc[c] += ww * r[f * DIM + c];
+        for (int c = 0; c < DIM; ++c) acc[c] += ww * v[c];
       }
+  store_node<DIM>(bc, node, acc);
+  if (xc) {
+    const double w = *wp;
+    double d[DIM];
+    load_node<DIM>(dinvc, node, d);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) {
-    bc[node * DIM + c] = acc[c];
-    if (xc) xc[node * DIM + c] = w * dinvc[node * DIM + c] * acc[c];
+    for (int c = 0; c < DIM; ++c) d[c] = w * d[c] * acc[c];
+    store_node<DIM>(xc, node, d);
   }
 }
 
 // x += P e
 template <int DIM>
 __global__ void __launch_bounds__(TPB) k_prolong_add(Coarsening T, const double* __restrict__ e, double* __restrict__ x) {
-  const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (node >= T.F.n) return;
-  int i, j, k;
-  T.F.ijk(node, i, j, k);
-  int ix[2], iy[2], iz[2];
-  double wx[2], wy[2], wz[2];
-  const int nx = coarse_of_fine(i, T.co[0], ix, wx);
-  const int ny = coarse_of_fine(j, T.co[1], iy, wy);
-  const int nz = DIM == 3 ? coarse_of_fine(k, T.co[2], iz, wz) : 1;
-  if (DIM == 2) { iz[0] = 0; wz[0] = 1.0; }
-  double acc[DIM];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z * blockDim.z + threadIdx.z;
+  if (!(i < T.F.nn[0] && j < T.F.nn[1] && k < T.F.nn[2])) return;
+  const int node = T.F.id(i, j, k);
+  double pe[DIM], xv[DIM];
+  prolong_at<DIM>(T, e, i, j, k, pe);
+  load_node<DIM>(x, node, xv);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
-  for (int c2 = 0; c2 < nz; ++c2)
-    for (int b = 0; b < ny; ++b)
-      for (int a = 0; a < nx; ++a) {
-        const double ww = wx[a] * wy[b] * wz[c2];
-        const long long m = T.C.id(ix[a], iy[b], iz[c2]);
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) acc[c] += ww * e[m * DIM + c];
-      }
-#pragma unroll
-  for (int c = 0; c < DIM; ++c) x[node * DIM + c] += acc[c];
+  for (int c = 0; c < DIM; ++c) xv[c] += pe[c];
+  store_node<DIM>(x, node, xv);
 }
 
 // Galerkin product A_c = P^T A P into stencil storage; one thread per
 // (coarse node, stencil slot).  The fine operator is read through its block()
 // provider, so level 0 is never assembled.
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_rap(Op op, Coarsening T, double* __restrict__ Ac) {
-  extern __shared__ double tmg_smem[];
-  op.init(tmg_smem);
-  __syncthreads();
+__global__ void __launch_bounds__(TPB) k_rap(const __grid_constant__ Op op, Coarsening T, double* __restrict__ Ac) {
   constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= T.C.n * NS) return;

@@ -5,7 +5,13 @@
 // [x+=alpha p, r-=alpha q, r.r] [convergence check -> cudaGraphSetConditional].
 // No host round trip per iteration; dot products use deterministic two-level
 // reductions so the iterate sequence is bitwise reproducible.
+//
+// TMG_PCG_EAGER=1 runs the same kernels without the graph (one host check per
+// iteration) -- used for per-kernel profiling, which cannot see inside
+// conditional graph bodies.
 #pragma once
+#include <cstdlib>
+
 #include "tmg_gmg.cuh"
 
 namespace tmg {
@@ -16,11 +22,12 @@ struct CgCfg {
 };
 struct CgState {
   double rz, tol;
-  int it, converged;
+  int it, converged, go;
 };
 
 __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ bb,
-                          const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h) {
+                          const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h,
+                          int use_cond) {
   const double tol = cfg->rtol * sqrt(*bb);
   const double r0 = sqrt(*rr);
   st->tol = tol;
@@ -28,37 +35,40 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
   st->rz = 0.0;
   hist[0] = r0;
   st->converged = r0 <= tol;
-  cudaGraphSetConditional(h, (!(r0 <= tol) && cfg->maxit > 0) ? 1u : 0u);
+  st->go = (!(r0 <= tol) && cfg->maxit > 0) ? 1 : 0;
+  if (use_cond) cudaGraphSetConditional(h, st->go ? 1u : 0u);
 }
 
+// p' = z + beta p (own node and, on the fly, its neighbours); q = A p'; reduce p'.q
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_cg_pq(Op op, const double* __restrict__ z, const double* __restrict__ p,
-                                               double* __restrict__ pn, double* __restrict__ q,
-                                               const CgState* __restrict__ st, const double* __restrict__ rz_new,
-                                               Red red) {
-  TMG_NODE_PROLOGUE
+__global__ void __launch_bounds__(TPB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
+                                               const double* __restrict__ p, double* __restrict__ pn,
+                                               double* __restrict__ q, const CgState* __restrict__ st,
+                                               const double* __restrict__ rz_new, Red red) {
+  TMG_NODE_IDX
   const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
   double v = 0.0;
   if (active) {
-    AxpySrc<DIM> src{z, p, beta};
-    double out[DIM];
-    op.row(node, ci, cj, ck, src, out);
+    double out[DIM], pv[DIM];
+    op.row(node, ci, cj, ck, AxpySrc<DIM>{z, p, beta}, out, pv);
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-      const double pv = src(node, c);
-      pn[node * DIM + c] = pv;
-      q[node * DIM + c] = out[c];
-      v += pv * out[c];
-    }
+    for (int c = 0; c < DIM; ++c) v += pv[c] * out[c];
+    store_node<DIM>(pn, node, pv);
+    store_node<DIM>(q, node, out);
   }
   grid_reduce(v, red);
 }
 
+// x += alpha p'; r -= alpha q; p = p'; reduce r.r.  With z0: also the first
+// zero-start Jacobi sweep of the next V-cycle, z0 = w D0^-1 r.
 __global__ void __launch_bounds__(TPB) k_cg_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
                                                    const double* __restrict__ pn, const double* __restrict__ q,
                                                    long long n, const double* __restrict__ rz_new,
-                                                   const double* __restrict__ pq, Red red) {
+                                                   const double* __restrict__ pq, Red red,
+                                                   const double* __restrict__ dinv0, const double* __restrict__ wp0,
+                                                   double* __restrict__ z0) {
   const double alpha = *rz_new / *pq;
+  const double w0 = z0 ? *wp0 : 0.0;
   double v = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double pv = pn[i];
@@ -66,13 +76,15 @@ __global__ void __launch_bounds__(TPB) k_cg_update(double* __restrict__ x, doubl
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
     p[i] = pv;
+    if (z0) z0[i] = w0 * (dinv0[i] * ri);
     v += ri * ri;
   }
   grid_reduce(v, red);
 }
 
 __global__ void k_cg_check(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ rz_new,
-                           const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h) {
+                           const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h,
+                           int use_cond) {
   st->rz = *rz_new;
   const int it = st->it + 1;
   st->it = it;
@@ -80,7 +92,8 @@ __global__ void k_cg_check(const CgCfg* __restrict__ cfg, CgState* __restrict__ 
   hist[it] = rn;
   const bool conv = rn <= st->tol;
   st->converged = conv;
-  cudaGraphSetConditional(h, (!conv && it < cfg->maxit) ? 1u : 0u);
+  st->go = (!conv && it < cfg->maxit) ? 1 : 0;
+  if (use_cond) cudaGraphSetConditional(h, st->go ? 1u : 0u);
 }
 
 struct PcgCtx {
@@ -104,11 +117,67 @@ struct PcgCtx {
   }
 };
 
+// first-sweep fusion is possible when the V-cycle starts with a point-Jacobi
+// sweep on level 0 (and level 0 is not itself the coarsest level)
+inline double* pcg_z0(PcgCtx& C, Hierarchy* H) {
+  return (H && H->fused() && H->last() > 0) ? H->first_dst(0, C.z.get()) : nullptr;
+}
+
+template <int DIM>
+void pcg_prologue(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0, cudaStream_t s,
+                  cudaGraphConditionalHandle h, int use_cond) {
+  const long long n = C.ndof;
+  const unsigned gv = std::min<unsigned>(grid_for(n), 1184);
+  auto op0 = K.template fine<DIM>();
+  if (use_x0) {
+    k_residual<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), 0, s>>>(op0, C.x.get(), C.b.get(),
+                                                                                       C.r.get());
+    note_launch();
+  } else {
+    TMG_CUDA(cudaMemsetAsync(C.x.get(), 0, n * sizeof(double), s));
+    TMG_CUDA(cudaMemcpyAsync(C.r.get(), C.b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  if (double* z0 = pcg_z0(C, H)) {
+    k_scale_vec<<<grid_for(n), TPB, 0, s>>>(C.r.get(), H->lv[0]->dinv.get(), H->lv[0]->wdev.get(), z0, n);
+    note_launch();
+  }
+  k_dot<<<gv, TPB, 0, s>>>(C.b.get(), C.b.get(), n, C.bb.red());
+  k_dot<<<gv, TPB, 0, s>>>(C.r.get(), C.r.get(), n, C.rr.red());
+  k_cg_init<<<1, 1, 0, s>>>(C.cfg.get(), C.st.get(), C.bb.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
+  note_launch(3);
+  TMG_CUDA(cudaGetLastError());
+}
+
+template <int DIM>
+void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGraphConditionalHandle h,
+              int use_cond) {
+  const long long n = C.ndof;
+  const unsigned gv = std::min<unsigned>(grid_for(n), 1184);
+  auto op0 = K.template fine<DIM>();
+  const double* z = C.r.get();
+  double* z0 = pcg_z0(C, H);
+  bool dot_done = false;
+  if (H) {
+    const Red rz = C.rz.red();
+    dot_done = vcycle<DIM>(*H, 0, C.r.get(), C.z.get(), s, z0 != nullptr, &rz);
+    z = C.z.get();
+  }
+  if (!dot_done) {
+    k_dot<<<gv, TPB, 0, s>>>(C.r.get(), z, n, C.rz.red());
+    note_launch();
+  }
+  k_cg_pq<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), 0, s>>>(
+      op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(), C.rz.res.get(), C.pq.red());
+  k_cg_update<<<gv, TPB, 0, s>>>(C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
+                                 C.pq.res.get(), C.rr.red(), z0 ? H->lv[0]->dinv.get() : nullptr,
+                                 z0 ? H->lv[0]->wdev.get() : nullptr, z0);
+  k_cg_check<<<1, 1, 0, s>>>(C.cfg.get(), C.st.get(), C.rz.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
+  note_launch(3);
+  TMG_CUDA(cudaGetLastError());
+}
+
 template <int DIM>
 void pcg_build_graph(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0) {
-  const long long n = C.ndof;
-  const unsigned gn = grid_for(K.L.n);
-  const unsigned gv = std::min<unsigned>(grid_for(n), 1184);
   if (C.exec) { cudaGraphExecDestroy(C.exec); C.exec = nullptr; }
   cudaStream_t s = C.cs;
   TMG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -119,21 +188,9 @@ void pcg_build_graph(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0) {
   TMG_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps));
   cudaGraphConditionalHandle handle;
   TMG_CUDA(cudaGraphConditionalHandleCreate(&handle, g, 0, 0));
-  auto op0 = K.template fine<DIM>();
   const long long c0 = launch_counter().load();
-  // prologue
-  if (use_x0) {
-    k_residual<DIM, decltype(op0)><<<gn, TPB, smem_of(op0), s>>>(op0, C.x.get(), C.b.get(), C.r.get()); ::tmg::note_launch();
-  } else {
-    TMG_CUDA(cudaMemsetAsync(C.x.get(), 0, n * sizeof(double), s));
-    TMG_CUDA(cudaMemcpyAsync(C.r.get(), C.b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  }
-  k_dot<<<gv, TPB, 0, s>>>(C.b.get(), C.b.get(), n, C.bb.red()); ::tmg::note_launch();
-  k_dot<<<gv, TPB, 0, s>>>(C.r.get(), C.r.get(), n, C.rr.red()); ::tmg::note_launch();
-  k_cg_init<<<1, 1, 0, s>>>(C.cfg.get(), C.st.get(), C.bb.res.get(), C.rr.res.get(), C.hist.get(), handle); ::tmg::note_launch();
-  TMG_CUDA(cudaGetLastError());
+  pcg_prologue<DIM>(C, K, H, use_x0, s, handle, 1);
   const long long c1 = launch_counter().load();
-  // while node
   TMG_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
@@ -144,26 +201,14 @@ void pcg_build_graph(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0) {
   TMG_CUDA(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   TMG_CUDA(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
-  cudaStream_t b2 = C.cs2;
-  TMG_CUDA(cudaStreamBeginCaptureToGraph(b2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  const double* z = C.r.get();
-  if (H) {
-    vcycle<DIM>(*H, 0, C.r.get(), C.z.get(), b2);
-    z = C.z.get();
-  }
-  k_dot<<<gv, TPB, 0, b2>>>(C.r.get(), z, n, C.rz.red()); ::tmg::note_launch();
-  k_cg_pq<DIM, decltype(op0)><<<gn, TPB, smem_of(op0), b2>>>(op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(),
-                                                             C.rz.res.get(), C.pq.red()); ::tmg::note_launch();
-  k_cg_update<<<gv, TPB, 0, b2>>>(C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
-                                  C.pq.res.get(), C.rr.red()); ::tmg::note_launch();
-  k_cg_check<<<1, 1, 0, b2>>>(C.cfg.get(), C.st.get(), C.rz.res.get(), C.rr.res.get(), C.hist.get(), handle); ::tmg::note_launch();
-  TMG_CUDA(cudaGetLastError());
+  TMG_CUDA(cudaStreamBeginCaptureToGraph(C.cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  pcg_body<DIM>(C, K, H, C.cs2, handle, 1);
   const long long c2 = launch_counter().load();
   C.prologue_launches = c1 - c0;
   C.body_launches = c2 - c1;
   note_launch(-(c2 - c0));  // captured, not executed
   cudaGraph_t body_out = nullptr;
-  TMG_CUDA(cudaStreamEndCapture(b2, &body_out));
+  TMG_CUDA(cudaStreamEndCapture(C.cs2, &body_out));
   cudaGraph_t gout = nullptr;
   TMG_CUDA(cudaStreamEndCapture(s, &gout));
   TMG_CUDA(cudaGraphInstantiate(&C.exec, gout, 0));
@@ -177,6 +222,11 @@ struct PcgResult {
   std::vector<double> hist;
 };
 
+inline bool pcg_eager() {
+  const char* e = std::getenv("TMG_PCG_EAGER");
+  return e && e[0] == '1';
+}
+
 template <int DIM>
 PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy* H, const double* b, double* x,
                     bool use_x0, double rtol, int maxit, cudaStream_t user) {
@@ -185,10 +235,11 @@ PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy*
   if (!slot) slot = std::make_unique<PcgCtx>();
   PcgCtx& C = *slot;
   const long long n = K.ndof;
+  const bool eager = pcg_eager();
   bool rebuild = C.exec == nullptr || C.use_x0_graph != use_x0;
   if (C.ndof != n) {
     C.ndof = n;
-    const unsigned gmax = std::max(grid_for(K.L.n), 1184u);
+    const unsigned gmax = std::max(node_blocks(node_grid<DIM>(K.L)), 1184u);
     cudaStream_t s = user;
     C.b.alloc(n, s); C.x.alloc(n, s); C.r.alloc(n, s); C.z.alloc(n, s);
     C.p.alloc(n, s); C.pn.alloc(n, s); C.q.alloc(n, s);
@@ -205,22 +256,32 @@ PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy*
     C.hist.alloc(C.hist_cap, user);
     rebuild = true;
   }
-  if (rebuild) {
+  if (rebuild && !eager) {
     TMG_CUDA(cudaStreamSynchronize(user));  // buffers allocated on `user` must exist before capture
     pcg_build_graph<DIM>(C, K, H, use_x0);
   }
   CgCfg hc{rtol, maxit};
+  CgState hs;
   TMG_CUDA(cudaEventRecord(C.e0, user));
   TMG_CUDA(cudaMemcpyAsync(C.cfg.get(), &hc, sizeof(hc), cudaMemcpyHostToDevice, user));
   TMG_CUDA(cudaMemcpyAsync(C.b.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, user));
   if (use_x0) TMG_CUDA(cudaMemcpyAsync(C.x.get(), x, n * sizeof(double), cudaMemcpyDeviceToDevice, user));
-  TMG_CUDA(cudaGraphLaunch(C.exec, user));
+  if (eager) {
+    pcg_prologue<DIM>(C, K, H, use_x0, user, 0, 0);
+    while (true) {
+      TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
+      TMG_CUDA(cudaStreamSynchronize(user));
+      if (!hs.go) break;
+      pcg_body<DIM>(C, K, H, user, 0, 0);
+    }
+  } else {
+    TMG_CUDA(cudaGraphLaunch(C.exec, user));
+  }
   TMG_CUDA(cudaMemcpyAsync(x, C.x.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, user));
   TMG_CUDA(cudaEventRecord(C.e1, user));
-  CgState hs;
   TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
   TMG_CUDA(cudaStreamSynchronize(user));
-  note_launch(C.prologue_launches + (long long)hs.it * C.body_launches);
+  if (!eager) note_launch(C.prologue_launches + (long long)hs.it * C.body_launches);
   PcgResult res;
   res.iterations = hs.it;
   res.converged = hs.converged;

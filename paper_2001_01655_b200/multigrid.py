@@ -33,12 +33,15 @@ class SmootherConfig:
     block_size: int = 2
     lanczos_steps: int = 10
     seed: int = 0
+    safeguard: float = 0.0  # weighted_jacobi: cap w at safeguard/lambda_hat per level (0 = off)
 
     def __post_init__(self):
         if not (0 < self.weight <= 1):
             raise ValueError("smoother weight must be in (0, 1]")
         if self.inner_iterations < 1:
             raise ValueError("inner_iterations must be >= 1")
+        if self.safeguard and (self.kind != "weighted_jacobi" or not 0 < self.safeguard < 2):
+            raise ValueError("safeguard applies to weighted_jacobi only and must be in (0, 2)")
 
     @property
     def stationary(self):
@@ -53,6 +56,7 @@ class SmootherConfig:
         d.inner_iterations = int(self.inner_iterations)
         d.lanczos_steps = int(self.lanczos_steps)
         d.seed = int(self.seed)
+        d.safeguard = float(self.safeguard)
         return d
 
 
