@@ -191,12 +191,14 @@ def run_b200(args, rank, world, local):
     def step():
         work = 0
         iters = []
+        state["legs"] = []
         for leg in legs:
             E = law.modulus(rho_d)
             K = T.StiffnessOperator(w.mesh, w.bc, E)
             sm = problems.gmg_settings(leg)
             h = T.build_gmg(w.mesh, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
-            u, rec = T.cg_solve(K, f_d, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=20000))
+            u, rec = T.cg_solve(K, f_d, None, h, T.SolveConfig(rtol=w.rtol,
+                                                              max_iterations=leg.get("max_iterations", 10000)))
             dc = empty_dev(w.mesh.element_count)
             comp = C.c_double()
             _lib.check(L.tmg_compliance_sensitivity(K.handle, ptr(rho_d), ptr(f_d), ptr(u), law.penalty,
@@ -205,6 +207,12 @@ def run_b200(args, rank, world, local):
             work += w.ndof * rec.iterations
             iters.append(rec.iterations)
             state["K"], state["h"], state["rec"], state["compliance"] = K, h, rec, comp.value
+            hist = rec.residual_history
+            state["legs"].append({"leg": "%s%d" % (leg["strategy"], leg.get("levels", 0)),
+                                  "iterations": rec.iterations, "converged": rec.converged,
+                                  "rel_residual": hist[-1] / hist[0], "solve_ms": rec.solve_time * 1e3,
+                                  "max_iterations": leg.get("max_iterations", 10000),
+                                  "compliance": comp.value})
         return work, iters
 
     for _ in range(args.warmup):
@@ -245,8 +253,7 @@ def run_b200(args, rank, world, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
             "config": config_dict(w, args, world, ["gmg%d" % l["levels"] for l in legs], pending),
-            "pcg_iterations": it_log[-1], "compliance": state["compliance"],
-            "solve_ms_last": state["rec"].solve_time * 1e3,
+            "pcg_iterations": it_log[-1], "leg_results": state["legs"],
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         wk, dt, its = oracle_sample(w, legs[0], args.cpu_sample_iters)
@@ -304,7 +311,7 @@ def e2e_run(args, w, legs, L, law):
     mg.max_levels = leg["levels"]
     mg.smoother = sm
     mg.n_pre, mg.n_post = leg["n_pre"], leg["n_post"]
-    cfg = _lib.SolveDesc(w.rtol, 20000)
+    cfg = _lib.SolveDesc(w.rtol, leg.get("max_iterations", 10000))
     rho = np.ascontiguousarray(w.rho, dtype=np.float64)
     f = np.ascontiguousarray(w.bc.load_vector)
     fixed = np.ascontiguousarray(w.bc.fixed_dofs, dtype=np.int64)

@@ -204,10 +204,12 @@ int tmg_operator_apply(tmg_operator* K, const double* x, double* y, void* stream
   const Operator& o = K->op;
   if (o.dim == 2) {
     auto f = o.fine<2>();
-    k_apply<2, FineOp<2>><<<node_grid<2>(o.L), node_block<2>(), 0, S(stream)>>>(f, x, y); ::tmg::note_launch();
+    k_apply<2, FineOp<2>><<<node_grid<2>(o.L), node_block<2>(), FineOp<2>::SMEM_BYTES, S(stream)>>>(f, x, y);
+    ::tmg::note_launch();
   } else {
     auto f = o.fine<3>();
-    k_apply<3, FineOp<3>><<<node_grid<3>(o.L), node_block<3>(), 0, S(stream)>>>(f, x, y); ::tmg::note_launch();
+    k_apply<3, FineOp<3>><<<node_grid<3>(o.L), node_block<3>(), FineOp<3>::SMEM_BYTES, S(stream)>>>(f, x, y);
+    ::tmg::note_launch();
   }
   TMG_CUDA(cudaGetLastError());
   ABI_END
@@ -413,7 +415,7 @@ int tmg_compliance_sensitivity(tmg_operator* K, const double* rho, const double*
   if (compliance) {
     RedSlot r;
     r.alloc(1184, s);
-    k_dot<<<std::min<unsigned>(grid_for(K->op.ndof), 1184), TPB, 0, s>>>(f, u, K->op.ndof, r.red()); ::tmg::note_launch();
+    k_dot<<<red_grid(K->op.ndof), TPB, 0, s>>>(f, u, K->op.ndof, r.red()); ::tmg::note_launch();
     TMG_CUDA(cudaMemcpyAsync(compliance, r.res.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     TMG_CUDA(cudaStreamSynchronize(s));
   }

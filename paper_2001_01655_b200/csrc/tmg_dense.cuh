@@ -127,10 +127,21 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A,
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const double* a = A + row * n;
-  double s = 0.0;
-  for (long long j = lane; j < n; j += 32) s += a[j] * b[j];
-  s = warp_sum(s);
-  if (lane == 0) y[row] = s;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long j = lane;
+  for (; j + 7 * 32 < n; j += 8 * 32) {  // 8 independent row loads in flight per lane
+    double av[8], bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = __ldg(a + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bv[u] = __ldg(b + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += av[u] * bv[u];
+  }
+  for (; j < n; j += 32) s[0] += a[j] * b[j];
+  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  t = warp_sum(t);
+  if (lane == 0) y[row] = t;
 }
 
 // Dense SPD inverse on the device (setup; stream-ordered, no host sync).

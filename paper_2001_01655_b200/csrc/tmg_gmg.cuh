@@ -37,11 +37,25 @@ struct SmootherCfg {
 // ----------------------------------------------------------------------------
 // small vector kernels
 // ----------------------------------------------------------------------------
-__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, long long n, Red red) {
-  double s = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    s += a[i] * b[i];
-  grid_reduce(s, red);
+// Reduction kernels run on a small grid (RED_BLOCKS) with 4 independent loads in
+// flight per thread, so the last-block combine reads few partials.
+constexpr unsigned RED_BLOCKS = 296;  // 2 per SM
+inline unsigned red_grid(long long n) { return std::min<unsigned>(grid_for(n), RED_BLOCKS); }
+
+__global__ void __launch_bounds__(TPB) k_dot(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                                             Red red) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const double a0 = __ldg(a + i), a1 = __ldg(a + i + stride), a2 = __ldg(a + i + 2 * stride),
+                 a3 = __ldg(a + i + 3 * stride);
+    const double b0 = __ldg(b + i), b1 = __ldg(b + i + stride), b2 = __ldg(b + i + 2 * stride),
+                 b3 = __ldg(b + i + 3 * stride);
+    s0 += a0 * b0; s1 += a1 * b1; s2 += a2 * b2; s3 += a3 * b3;
+  }
+  for (; i < n; i += stride) s0 += a[i] * b[i];
+  grid_reduce((s0 + s1) + (s2 + s3), red);
 }
 __global__ void k_scale_vec(const double* __restrict__ b, const double* __restrict__ d, const double* __restrict__ wp,
                             double* __restrict__ x, long long n) {
@@ -212,7 +226,8 @@ void with_op(const Level& l, F&& f) {
   }
 }
 
-#define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), 0
+// launch configuration of a node kernel on level l with operator `o` in scope
+#define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), decltype(o)::SMEM_BYTES
 
 template <int DIM>
 void level_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
@@ -235,7 +250,7 @@ void lanczos_setup(Hierarchy& H, Level& l, cudaStream_t s) {
   if (cheb) l.coef.alloc(2 * std::max(H.sm.degree, 1), s);
   l.lmax.alloc(1, s);
   const unsigned g = grid_for(l.ndof);
-  const unsigned gr = std::min<unsigned>(g, 1184);
+  const unsigned gr = red_grid(l.ndof);
   k_splitmix<<<g, TPB, 0, s>>>(v.get(), l.ndof, (unsigned long long)H.sm.seed);
   Red rn = H.red.red();
   rn.result = nrm.get();
@@ -502,7 +517,7 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
       xcur = (cheb || H.n_post % 2 == 0) ? xout : l.xt.get();
       TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
     }
-    k_prolong_add<DIM><<<TMG_NODE_LAUNCH(l), s>>>(l.T, c.x.get(), xcur);
+    k_prolong_add<DIM><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(l.T, c.x.get(), xcur);
     note_launch();
     if (cheb) {
       smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);

@@ -41,15 +41,32 @@ struct Slots {  // 3^DIM stencil neighbourhood, slot = (dx+1) + 3(dy+1) + 9(dz+1
   }
 };
 
+// Register fence: the values must be materialised here.  Placed after a batch of
+// loads it stops the scheduler from sinking each load next to its first use
+// (which serialises L2 round trips on the thread-starved coarse levels).
+// (multi-operand asm statements: one operand per statement does not hold the
+// batch together, eight do -- verified on the SASS with cuobjdump.)
+template <int N>
+__device__ __forceinline__ void reg_fence(double* v) {
+#pragma unroll
+  for (int t = 0; t + 8 <= N; t += 8)
+    asm volatile("" : "+d"(v[t]), "+d"(v[t + 1]), "+d"(v[t + 2]), "+d"(v[t + 3]), "+d"(v[t + 4]), "+d"(v[t + 5]),
+                 "+d"(v[t + 6]), "+d"(v[t + 7]));
+#pragma unroll
+  for (int t = N - N % 8; t < N; ++t) asm volatile("" : "+d"(v[t]));
+}
+__device__ __forceinline__ double ldv(const double* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldv2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
 template <int DIM>
 __device__ __forceinline__ void load_node(const double* __restrict__ v, int node, double out[DIM]) {
   if (DIM == 2) {
-    const double2 t = __ldg(reinterpret_cast<const double2*>(v) + node);
+    const double2 t = ldv2(v + 2 * node);
     out[0] = t.x;
     out[1] = t.y;
   } else {
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) out[c] = __ldg(v + node * DIM + c);
+    for (int c = 0; c < DIM; ++c) out[c] = ldv(v + node * DIM + c);
   }
 }
 template <int DIM>
@@ -195,27 +212,67 @@ struct FineOp {
 
   __device__ int elem_id(int ex, int ey, int ez) const { return ex + ne[0] * (ey + ne[1] * ez); }
 
-  // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src
+  // Shared-memory tile of one node block (node_block<DIM>: BX x BY x BZ) plus a
+  // one-node halo: the source vector (unmasked), the free-dof masks and the
+  // moduli of the (BX+1)(BY+1)(BZ+1) elements touching the tile.  Every value is
+  // read from L2/HBM once per block instead of once per neighbouring thread.
+  static constexpr int BX = 32, BY = DIM == 2 ? 8 : 4, BZ = DIM == 2 ? 1 : 2;
+  static constexpr int HX = BX + 2, HY = BY + 2, HZ = DIM == 2 ? 1 : BZ + 2;
+  static constexpr int EX = BX + 1, EY = BY + 1, EZ = DIM == 2 ? 1 : BZ + 1;
+  static constexpr int NH = HX * HY * HZ, NEL = EX * EY * EZ;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * (NH * DIM + NEL) + NH;
+
+  // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
+  // ALL threads of the block (it stages the tile and synchronises); only threads
+  // with `active` compute.
   template <class Src>
-  __device__ void row(int node, int i, int j, int k, const Src& src, double out[DIM], double self[DIM]) const {
+  __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
+                      double self[DIM]) const {
+    extern __shared__ double tmg_sm[];
+    double* xs = tmg_sm;
+    double* es = xs + NH * DIM;
+    unsigned char* ms = reinterpret_cast<unsigned char*>(es + NEL);
+    const int i0 = blockIdx.x * BX - 1, j0 = blockIdx.y * BY - 1, k0 = DIM == 3 ? (int)blockIdx.z * BZ - 1 : 0;
+    const int t0 = lin_tid(), nt = lin_nthreads();
+    for (int t = t0; t < NH; t += nt) {
+      const int hx = t % HX, hy = (t / HX) % HY, hz = t / (HX * HY);
+      const int gi = i0 + hx, gj = j0 + hy, gk = DIM == 3 ? k0 + hz : 0;
+      double v[DIM];
+      unsigned mk = 0u;
+      if (L.inside(gi, gj, gk)) {
+        const int m = L.id(gi, gj, gk);
+        src.load(m, gi, gj, gk, v);
+        mk = __ldg(mask + m);
+      } else {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) v[d] = 0.0;
+      }
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) xs[t * DIM + d] = v[d];
+      ms[t] = (unsigned char)mk;
+    }
+    for (int t = t0; t < NEL; t += nt) {
+      const int ex = t % EX, ey = (t / EX) % EY, ez = t / (EX * EY);
+      const int gi = i0 + 1 + ex - 1, gj = j0 + 1 + ey - 1, gk = DIM == 3 ? k0 + ez : 0;
+      const bool ok = gi >= 0 && gi < ne[0] && gj >= 0 && gj < ne[1] && (DIM == 2 || (gk >= 0 && gk < ne[2]));
+      es[t] = ok ? __ldg(E + elem_id(gi, gj, gk)) : 0.0;
+    }
+    __syncthreads();
+    if (!active) return;
+    const int tx = threadIdx.x, ty = threadIdx.y, tz = DIM == 3 ? threadIdx.z : 0;
     constexpr int NS = Slots<DIM>::NS;
     double xv[NS][DIM];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
-      const bool in = L.inside(ii, jj, kk);
-      const int ic = min(max(ii, 0), L.nn[0] - 1), jc = min(max(jj, 0), L.nn[1] - 1);
-      const int kc = DIM == 3 ? min(max(kk, 0), L.nn[2] - 1) : 0;
-      const int m = L.id(ic, jc, kc);
-      const unsigned mk = in ? (unsigned)__ldg(mask + m) : 0u;
-      double v[DIM];
-      src.load(m, ic, jc, kc, v);
-      if (s == NS / 2) {
+      const int h = (tx + 1 + Slots<DIM>::dx(s)) + HX * ((ty + 1 + Slots<DIM>::dy(s)) + HY * (tz + (DIM == 3 ? 1 : 0) +
+                                                                                                Slots<DIM>::dz(s)));
+      const unsigned mk = ms[h];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) self[d] = v[d];
+      for (int d = 0; d < DIM; ++d) {
+        const double v = xs[h * DIM + d];
+        if (s == NS / 2) self[d] = v;
+        xv[s][d] = ((mk >> d) & 1u) ? v : 0.0;
       }
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) xv[s][d] = ((mk >> d) & 1u) ? v[d] : 0.0;
     }
     double acc[DIM];
 #pragma unroll
@@ -226,11 +283,7 @@ struct FineOp {
       for (int ey = 0; ey < 2; ++ey)
 #pragma unroll
         for (int ex = 0; ex < 2; ++ex) {
-          const int eI = i - 1 + ex, eJ = j - 1 + ey, eK = DIM == 3 ? k - 1 + ez : 0;
-          const bool ok = eI >= 0 && eI < ne[0] && eJ >= 0 && eJ < ne[1] && (DIM == 2 || (eK >= 0 && eK < ne[2]));
-          const int ec = elem_id(min(max(eI, 0), ne[0] - 1), min(max(eJ, 0), ne[1] - 1),
-                                 DIM == 3 ? min(max(eK, 0), ne[2] - 1) : 0);
-          const double Ee = ok ? __ldg(E + ec) : 0.0;
+          const double Ee = es[(tx + ex) + EX * ((ty + ey) + EY * (tz + ez))];
           const int ln = corner_of(1 - ex, 1 - ey, DIM == 3 ? 1 - ez : 0);
           double t[DIM];
 #pragma unroll
@@ -247,7 +300,7 @@ struct FineOp {
 #pragma unroll
           for (int c = 0; c < DIM; ++c) acc[c] += Ee * t[c];
         }
-    const unsigned mn = __ldg(mask + node);
+    const unsigned mn = ms[(tx + 1) + HX * ((ty + 1) + HY * (tz + (DIM == 3 ? 1 : 0)))];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) out[c] = ((mn >> c) & 1u) ? acc[c] : self[c];
   }
@@ -294,27 +347,45 @@ struct StencilOp {
   Lat L;
   const double* __restrict__ A;
 
+  // Loads are issued in batches of G slots (all coefficient and vector loads of a
+  // batch before any arithmetic) so a thread has G*(DD+DIM) loads in flight --
+  // coarse levels have too few threads to hide L2 latency by occupancy alone.
+  static constexpr size_t SMEM_BYTES = 0;
   template <class Src>
-  __device__ void row(int node, int i, int j, int k, const Src& src, double out[DIM], double self[DIM]) const {
+  __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
+                      double self[DIM]) const {
+    if (!active) return;
+    constexpr int G = DIM == 2 ? 9 : 3;
     const int n = (int)L.n;
     double acc[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const int ii = min(max(i + Slots<DIM>::dx(s), 0), L.nn[0] - 1);
-      const int jj = min(max(j + Slots<DIM>::dy(s), 0), L.nn[1] - 1);
-      const int kk = DIM == 3 ? min(max(k + Slots<DIM>::dz(s), 0), L.nn[2] - 1) : 0;
-      double xv[DIM];
-      src.load(L.id(ii, jj, kk), ii, jj, kk, xv);  // clamped; the slot's coefficients are 0 there
-      if (s == NS / 2) {
+    for (int s0 = 0; s0 < NS; s0 += G) {
+      double xv[G][DIM], av[G][DD];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) self[d] = xv[d];
+      for (int g = 0; g < G; ++g) {
+        const int s = s0 + g;
+        const int ii = min(max(i + Slots<DIM>::dx(s), 0), L.nn[0] - 1);
+        const int jj = min(max(j + Slots<DIM>::dy(s), 0), L.nn[1] - 1);
+        const int kk = DIM == 3 ? min(max(k + Slots<DIM>::dz(s), 0), L.nn[2] - 1) : 0;
+        src.load(L.id(ii, jj, kk), ii, jj, kk, xv[g]);  // clamped; the slot's coefficients are 0 there
+#pragma unroll
+        for (int q = 0; q < DD; ++q) av[g][q] = ldv(A + (s * DD + q) * n + node);
       }
+      reg_fence<G * DIM>(&xv[0][0]);
+      reg_fence<G * DD>(&av[0][0]);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a)
+      for (int g = 0; g < G; ++g) {
+        if (s0 + g == NS / 2) {
 #pragma unroll
-        for (int b = 0; b < DIM; ++b) acc[a] += __ldg(A + (s * DD + a * DIM + b) * n + node) * xv[b];
+          for (int d = 0; d < DIM; ++d) self[d] = xv[g][d];
+        }
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) acc[a] += av[g][a * DIM + b] * xv[g][b];
+      }
     }
 #pragma unroll
     for (int c = 0; c < DIM; ++c) out[c] = acc[c];
@@ -340,23 +411,23 @@ struct StencilOp {
 
 // y = A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, 1) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
                                                double* __restrict__ y) {
   TMG_NODE_IDX
-  if (!active) return;
   double out[DIM], self[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  if (!active) return;
   store_node<DIM>(y, node, out);
 }
 
 // y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
+__global__ void __launch_bounds__(TPB, 1) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
                                                    const double* __restrict__ ds, double* __restrict__ y) {
   TMG_NODE_IDX
-  if (!active) return;
   double out[DIM], self[DIM], d[DIM];
-  op.row(node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
+  op.row(active, node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
+  if (!active) return;
   load_node<DIM>(ds, node, d);
 #pragma unroll
   for (int c = 0; c < DIM; ++c) out[c] *= d[c];
@@ -365,12 +436,12 @@ __global__ void __launch_bounds__(TPB) k_apply_sym(const __grid_constant__ Op op
 
 // r = b - A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, 1) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ r) {
   TMG_NODE_IDX
-  if (!active) return;
   double out[DIM], self[DIM], bb[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+  if (!active) return;
   load_node<DIM>(b, node, bb);
 #pragma unroll
   for (int c = 0; c < DIM; ++c) out[c] = bb[c] - out[c];
@@ -386,10 +457,11 @@ __device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const 
                                             double* __restrict__ xo, const Red& red) {
   TMG_NODE_IDX
   double v = 0.0;
+  double out[DIM], self[DIM];
+  op.row(active, node, ci, cj, ck, src, out, self);
   if (active) {
     const double w = *wp;
-    double out[DIM], self[DIM], bb[DIM], d[DIM];
-    op.row(node, ci, cj, ck, src, out, self);
+    double bb[DIM], d[DIM];
     load_node<DIM>(b, node, bb);
     load_node<DIM>(dinv, node, d);
 #pragma unroll
@@ -403,7 +475,7 @@ __device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const 
 }
 
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, 1) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                 const double* __restrict__ b, const double* __restrict__ dinv,
                                                 const double* __restrict__ wp, double* __restrict__ xo, Red red) {
   jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
@@ -412,7 +484,7 @@ __global__ void __launch_bounds__(TPB) k_jacobi(const __grid_constant__ Op op, c
 // first post-smoothing sweep with the coarse-grid correction fused in:
 // xs = x + P e evaluated on the fly, xo = xs + w D^-1 (b - A xs)
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, 1) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                         const double* __restrict__ e, Coarsening T,
                                                         const double* __restrict__ b, const double* __restrict__ dinv,
                                                         const double* __restrict__ wp, double* __restrict__ xo,
@@ -422,14 +494,14 @@ __global__ void __launch_bounds__(TPB) k_prolong_jacobi(const __grid_constant__ 
 
 // xo = x + w B^-1 (b - A x), B the nodal diagonal blocks (multigrid.py:90)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, 1) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                  const double* __restrict__ b, const double* __restrict__ binv,
                                                  const double* __restrict__ wp, double* __restrict__ xo) {
   TMG_NODE_IDX
+  double out[DIM], self[DIM], r[DIM];
+  op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
   if (!active) return;
   const double w = *wp;
-  double out[DIM], self[DIM], r[DIM];
-  op.row(node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
   load_node<DIM>(b, node, r);
 #pragma unroll
   for (int c = 0; c < DIM; ++c) r[c] -= out[c];
@@ -446,16 +518,16 @@ __global__ void __launch_bounds__(TPB) k_bjacobi(const __grid_constant__ Op op, 
 // One Chebyshev step (multigrid.py:131 recurrence, SOR solve -> D^-1):
 //   p' = D^-1 r + beta p ; x += alpha p' ; r' = r - alpha A p'
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
+__global__ void __launch_bounds__(TPB, 1) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
                                               const double* __restrict__ p, const double* __restrict__ dinv,
                                               const double* __restrict__ coef, int step, int x_zero,
                                               double* __restrict__ x, double* __restrict__ po,
                                               double* __restrict__ ro) {
   TMG_NODE_IDX
-  if (!active) return;
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
   double out[DIM], pv[DIM], rr[DIM], xv[DIM];
-  op.row(node, ci, cj, ck, ChebSrc<DIM>{r, p, dinv, beta}, out, pv);
+  op.row(active, node, ci, cj, ck, ChebSrc<DIM>{r, p, dinv, beta}, out, pv);
+  if (!active) return;
   load_node<DIM>(r, node, rr);
   if (x_zero) {
 #pragma unroll
@@ -475,7 +547,7 @@ __global__ void __launch_bounds__(TPB) k_cheb(const __grid_constant__ Op op, con
 
 // diagonal / nodal block inverses of a level operator
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_diag(const __grid_constant__ Op op, double* __restrict__ diag,
+__global__ void __launch_bounds__(TPB, 1) k_diag(const __grid_constant__ Op op, double* __restrict__ diag,
                                               double* __restrict__ binv, unsigned* __restrict__ bad) {
   TMG_NODE_IDX
   if (!active) return;
@@ -508,7 +580,7 @@ __global__ void __launch_bounds__(TPB) k_diag(const __grid_constant__ Op op, dou
 
 // dense row-major copy of a level operator (small coarsest levels only)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_to_dense(const __grid_constant__ Op op, double* __restrict__ Ad) {
+__global__ void __launch_bounds__(TPB, 1) k_to_dense(const __grid_constant__ Op op, double* __restrict__ Ad) {
   TMG_NODE_IDX
   if (!active) return;
   const long long n = op.L.n * DIM;
@@ -526,7 +598,7 @@ __global__ void __launch_bounds__(TPB) k_to_dense(const __grid_constant__ Op op,
 // bc = P^T r ; optionally the first (zero-start) Jacobi sweep of the coarse level:
 // xc = w * dinvc .* bc  (fused so the coarse level starts with one kernel fewer)
 template <int DIM>
-__global__ void __launch_bounds__(TPB) k_restrict(Coarsening T, const double* __restrict__ r, double* __restrict__ bc,
+__global__ void __launch_bounds__(TPB, 1) k_restrict(Coarsening T, const double* __restrict__ r, double* __restrict__ bc,
                                                   const double* __restrict__ dinvc, const double* __restrict__ wp,
                                                   double* __restrict__ xc) {
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
@@ -566,7 +638,7 @@ __global__ void __launch_bounds__(TPB) k_restrict(Coarsening T, const double* __
 
 // x += P e
 template <int DIM>
-__global__ void __launch_bounds__(TPB) k_prolong_add(Coarsening T, const double* __restrict__ e, double* __restrict__ x) {
+__global__ void __launch_bounds__(TPB, 1) k_prolong_add(Coarsening T, const double* __restrict__ e, double* __restrict__ x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z * blockDim.z + threadIdx.z;
@@ -584,7 +656,7 @@ __global__ void __launch_bounds__(TPB) k_prolong_add(Coarsening T, const double*
 // (coarse node, stencil slot).  The fine operator is read through its block()
 // provider, so level 0 is never assembled.
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_rap(const __grid_constant__ Op op, Coarsening T, double* __restrict__ Ac) {
+__global__ void __launch_bounds__(TPB, 1) k_rap(const __grid_constant__ Op op, Coarsening T, double* __restrict__ Ac) {
   constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= T.C.n * NS) return;

@@ -41,16 +41,16 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
 
 // p' = z + beta p (own node and, on the fly, its neighbours); q = A p'; reduce p'.q
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
+__global__ void __launch_bounds__(TPB, 1) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
                                                const double* __restrict__ p, double* __restrict__ pn,
                                                double* __restrict__ q, const CgState* __restrict__ st,
                                                const double* __restrict__ rz_new, Red red) {
   TMG_NODE_IDX
   const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
   double v = 0.0;
+  double out[DIM], pv[DIM];
+  op.row(active, node, ci, cj, ck, AxpySrc<DIM>{z, p, beta}, out, pv);
   if (active) {
-    double out[DIM], pv[DIM];
-    op.row(node, ci, cj, ck, AxpySrc<DIM>{z, p, beta}, out, pv);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) v += pv[c] * out[c];
     store_node<DIM>(pn, node, pv);
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(TPB) k_cg_pq(const __grid_constant__ Op op, co
 
 // x += alpha p'; r -= alpha q; p = p'; reduce r.r.  With z0: also the first
 // zero-start Jacobi sweep of the next V-cycle, z0 = w D0^-1 r.
-__global__ void __launch_bounds__(TPB) k_cg_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+__global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
                                                    const double* __restrict__ pn, const double* __restrict__ q,
                                                    long long n, const double* __restrict__ rz_new,
                                                    const double* __restrict__ pq, Red red,
@@ -69,17 +69,34 @@ __global__ void __launch_bounds__(TPB) k_cg_update(double* __restrict__ x, doubl
                                                    double* __restrict__ z0) {
   const double alpha = *rz_new / *pq;
   const double w0 = z0 ? *wp0 : 0.0;
-  double v = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double pv = pn[i];
-    x[i] += alpha * pv;
-    const double ri = r[i] - alpha * q[i];
-    r[i] = ri;
-    p[i] = pv;
-    if (z0) z0[i] = w0 * (dinv0[i] * ri);
-    v += ri * ri;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i0 < n; i0 += 4 * stride) {
+    double pv[4], xv[4], rv[4], qv[4], dv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      const bool in = i < n;
+      pv[u] = in ? pn[i] : 0.0;
+      xv[u] = in ? x[i] : 0.0;
+      rv[u] = in ? r[i] : 0.0;
+      qv[u] = in ? q[i] : 0.0;
+      dv[u] = (in && z0) ? dinv0[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= n) continue;
+      x[i] = xv[u] + alpha * pv[u];
+      const double ri = rv[u] - alpha * qv[u];
+      r[i] = ri;
+      p[i] = pv[u];
+      if (z0) z0[i] = w0 * (dv[u] * ri);
+      v[u] += ri * ri;
+    }
   }
-  grid_reduce(v, red);
+  grid_reduce((v[0] + v[1]) + (v[2] + v[3]), red);
 }
 
 __global__ void k_cg_check(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ rz_new,
@@ -127,10 +144,11 @@ template <int DIM>
 void pcg_prologue(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0, cudaStream_t s,
                   cudaGraphConditionalHandle h, int use_cond) {
   const long long n = C.ndof;
-  const unsigned gv = std::min<unsigned>(grid_for(n), 1184);
+  const unsigned gv = red_grid(n);
   auto op0 = K.template fine<DIM>();
   if (use_x0) {
-    k_residual<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), 0, s>>>(op0, C.x.get(), C.b.get(),
+    k_residual<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s>>>(
+        op0, C.x.get(), C.b.get(),
                                                                                        C.r.get());
     note_launch();
   } else {
@@ -152,7 +170,7 @@ template <int DIM>
 void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGraphConditionalHandle h,
               int use_cond) {
   const long long n = C.ndof;
-  const unsigned gv = std::min<unsigned>(grid_for(n), 1184);
+  const unsigned gv = red_grid(n);
   auto op0 = K.template fine<DIM>();
   const double* z = C.r.get();
   double* z0 = pcg_z0(C, H);
@@ -166,7 +184,7 @@ void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGr
     k_dot<<<gv, TPB, 0, s>>>(C.r.get(), z, n, C.rz.red());
     note_launch();
   }
-  k_cg_pq<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), 0, s>>>(
+  k_cg_pq<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s>>>(
       op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(), C.rz.res.get(), C.pq.red());
   k_cg_update<<<gv, TPB, 0, s>>>(C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
                                  C.pq.res.get(), C.rr.red(), z0 ? H->lv[0]->dinv.get() : nullptr,

@@ -110,8 +110,12 @@ def config_1(seed=1655):
                     # levels 2-3 of this hierarchy (lambda 3.38, 3.51): the V-cycle is then
                     # indefinite and PCG cannot converge.  The bench leg caps the weight at
                     # 1.8/lambda_hat per level.
+                    # The thresholded field does not percolate (128 solid islands in void,
+                    # E contrast 5e8): GMG-PCG stagnates (rel. residual ~1e-4 after 20000
+                    # iterations), so the bench caps this leg at 2000 iterations and
+                    # reports the converged flag -- the paper's GMG failure mode.
                     solvers=[dict(strategy="gmg", levels=5, smoother="weighted_jacobi", weight=0.6,
-                                  n_pre=2, n_post=2, safeguard=1.8),
+                                  n_pre=2, n_post=2, safeguard=1.8, max_iterations=2000),
                              dict(strategy="amg", coarse_max_dofs=499, beta=0.08,
                                   smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2)])
 
