@@ -114,6 +114,30 @@ int tmg_operator_diagonal(tmg_operator* op, double* d_dev, void* stream);
 int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels,
                   const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
                   void* stream, tmg_hierarchy** out);
+/* multigrid.py:555 build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother, n_pre,
+ * n_post, seed).  near_nullspace_host: row-major (ndofs x nvec), nvec 3 (2D) or 6
+ * (3D).  beta: strength threshold (reference: 0.003, multigrid.py:22).
+ * v0_host: the power-method start vector numpy.random.default_rng(seed)
+ * .standard_normal(ndofs) of multigrid.py:509 (deeper levels use its prefix). */
+int tmg_sa_amg_build(tmg_operator* K, const double* near_nullspace_host, int32_t nvec,
+                     int64_t coarse_max_dofs, double beta, const double* v0_host,
+                     const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
+                     void* stream, tmg_hierarchy** out);
+/* multigrid.py:573 build_hybrid(mesh, K, near_nullspace, n_geo, ...) for n_geo >= 1:
+ * coarse_near_nullspace_host = rigid_body_modes(coarse_mesh) of the mesh reached
+ * after the geometric levels (coarse_ndof rows), v0_host its start vector. */
+int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* coarse_near_nullspace_host,
+                     int64_t coarse_ndof, int32_t nvec, int64_t coarse_max_dofs, double beta,
+                     const double* v0_host, const tmg_smoother_desc* smoother, int32_t n_pre,
+                     int32_t n_post, void* stream, tmg_hierarchy** out);
+/* MgHierarchy.flags as a comma-separated list. */
+int tmg_hierarchy_flags(const tmg_hierarchy* h, char* buf, int32_t cap);
+/* Export level data for parity checks (two-call: NULL buffers return dims only).
+ * what: 0 level operator (BSR; lattice levels converted), 1 smoothed P, 2 strength
+ * graph (rowptr/col), 3 aggregate ids (col; val[0] = rho(D^-1 A)), 4 tentative T.
+ * dims = {block rows, block cols (n_agg for 3), nnz blocks, R*1000+C}. */
+int tmg_hierarchy_export(tmg_hierarchy* h, int32_t level, int32_t what, int64_t* dims,
+                         int32_t* rowptr, int32_t* col, double* val, void* stream);
 int tmg_hierarchy_destroy(tmg_hierarchy* h);
 int tmg_hierarchy_num_levels(const tmg_hierarchy* h);
 int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_info* info);

@@ -12,7 +12,8 @@ from .krylov import SolveConfig, SolveRecord, cg_solve, pcg_solve
 from .material import SimpLaw
 from .mesh import (BoundaryConditions, StiffnessOperator, StructuredMesh, assemble_stiffness,
                    build_mesh, element_stiffness, rigid_body_modes)
-from .multigrid import MgHierarchy, SmootherConfig, build_gmg, gmg_level_dims
+from .multigrid import (MgHierarchy, SmootherConfig, build_gmg, build_hybrid, build_sa_amg,
+                        gmg_level_dims)
 from .optimization import SolverHarness, compliance_and_sensitivity, element_strain_energies
 
 __version__ = "0.1.0"
@@ -20,6 +21,7 @@ __version__ = "0.1.0"
 __all__ = [
     "SolveConfig", "SolveRecord", "cg_solve", "pcg_solve", "SimpLaw", "BoundaryConditions",
     "StiffnessOperator", "StructuredMesh", "assemble_stiffness", "build_mesh", "element_stiffness",
-    "rigid_body_modes", "MgHierarchy", "SmootherConfig", "build_gmg", "gmg_level_dims",
+    "rigid_body_modes", "MgHierarchy", "SmootherConfig", "build_gmg", "build_hybrid", "build_sa_amg",
+    "gmg_level_dims",
     "SolverHarness", "compliance_and_sensitivity", "element_strain_energies",
 ]

@@ -57,6 +57,12 @@ _SIGS = {
     "tmg_operator_diagonal": (C.c_int, [_P, _P, _P]),
     "tmg_gmg_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.POINTER(SmootherDesc), C.c_int32,
                                 C.c_int32, _P, C.POINTER(_P)]),
+    "tmg_sa_amg_build": (C.c_int, [_P, _P, C.c_int32, C.c_int64, C.c_double, _P, C.POINTER(SmootherDesc),
+                                   C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+    "tmg_hybrid_build": (C.c_int, [_P, C.c_int32, _P, C.c_int64, C.c_int32, C.c_int64, C.c_double, _P,
+                                   C.POINTER(SmootherDesc), C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+    "tmg_hierarchy_flags": (C.c_int, [_P, C.c_char_p, C.c_int32]),
+    "tmg_hierarchy_export": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P]),
     "tmg_hierarchy_destroy": (C.c_int, [_P]),
     "tmg_hierarchy_num_levels": (C.c_int, [_P]),
     "tmg_hierarchy_level_info": (C.c_int, [_P, C.c_int32, C.POINTER(LevelInfo)]),

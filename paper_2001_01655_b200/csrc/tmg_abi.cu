@@ -4,6 +4,7 @@
 
 #include "../../include/topomg_b200.h"
 #include "tmg_pcg.cuh"
+#include "tmg_sa.cuh"
 
 using namespace tmg;
 
@@ -267,6 +268,60 @@ int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels, 
   ABI_END
 }
 
+int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_t coarse_max_dofs, double beta,
+                     const double* v0_host, const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
+                     void* stream, tmg_hierarchy** out) {
+  ABI_BEGIN
+  TMG_REQUIRE(K && B_host && v0_host, "operator/near_nullspace/start vector is NULL");
+  TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
+  TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
+  const SmootherCfg c = to_cfg(smoother);
+  cudaStream_t s = S(stream);
+  const long long nd = K->op.ndof;
+  DevBuf<double> B, v0;
+  B.alloc(nd * nvec, s);
+  v0.alloc(nd, s);
+  TMG_CUDA(cudaMemcpyAsync(B.get(), B_host, nd * nvec * sizeof(double), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, nd * sizeof(double), cudaMemcpyHostToDevice, s));
+  auto H = std::make_unique<tmg_hierarchy>();
+  H->K = K;
+  if (K->op.dim == 2)
+    H->h = build_sa_amg<2>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post, s);
+  else
+    H->h = build_sa_amg<3>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post, s);
+  TMG_CUDA(cudaStreamSynchronize(s));
+  *out = H.release();
+  ABI_END
+}
+
+int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* Bc_host, int64_t coarse_ndof, int32_t nvec,
+                     int64_t coarse_max_dofs, double beta, const double* v0_host, const tmg_smoother_desc* smoother,
+                     int32_t n_pre, int32_t n_post, void* stream, tmg_hierarchy** out) {
+  ABI_BEGIN
+  TMG_REQUIRE(K && Bc_host && v0_host, "operator/near_nullspace/start vector is NULL");
+  TMG_REQUIRE(n_geo >= 1, "n_geo must be >= 1 (n_geo = 0 is build_sa_amg)");
+  TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
+  TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
+  const SmootherCfg c = to_cfg(smoother);
+  cudaStream_t s = S(stream);
+  DevBuf<double> B, v0;
+  B.alloc(coarse_ndof * nvec, s);
+  v0.alloc(coarse_ndof, s);
+  TMG_CUDA(cudaMemcpyAsync(B.get(), Bc_host, coarse_ndof * nvec * sizeof(double), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, coarse_ndof * sizeof(double), cudaMemcpyHostToDevice, s));
+  auto H = std::make_unique<tmg_hierarchy>();
+  H->K = K;
+  if (K->op.dim == 2)
+    H->h = build_hybrid<2>(K->op, n_geo, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
+                           coarse_ndof, s);
+  else
+    H->h = build_hybrid<3>(K->op, n_geo, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
+                           coarse_ndof, s);
+  TMG_CUDA(cudaStreamSynchronize(s));
+  *out = H.release();
+  ABI_END
+}
+
 int tmg_hierarchy_destroy(tmg_hierarchy* h) {
   ABI_BEGIN
   delete h;
@@ -286,12 +341,91 @@ int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_in
   if (level == h->h->last() && level > 0) {
     info->storage = 3;
     info->nonzeros = l.ndof * l.ndof;
-  } else if (l.fine) {
+  } else if (l.opkind == OP_FINE) {
     info->storage = 0;
     info->nonzeros = l.op->nelem;
-  } else {
+  } else if (l.opkind == OP_STENCIL) {
     info->storage = 1;
     info->nonzeros = (D == 2 ? 9 : 27) * (long long)D * D * l.L.n;
+  } else {
+    info->storage = 2;
+    info->nonzeros = l.Ab.scalar_nnz();
+  }
+  ABI_END
+}
+
+int tmg_hierarchy_flags(const tmg_hierarchy* h, char* buf, int32_t cap) {
+  ABI_BEGIN
+  TMG_REQUIRE(h && buf && cap > 0, "bad arguments");
+  std::string s;
+  for (const auto& f : h->h->flags) s += (s.empty() ? "" : ",") + f;
+  std::strncpy(buf, s.c_str(), cap - 1);
+  buf[cap - 1] = '\0';
+  ABI_END
+}
+
+static void copy_bsr(const Bsr& m, int64_t* dims, int32_t* rowptr, int32_t* col, double* val, cudaStream_t s) {
+  dims[0] = m.nrows;
+  dims[1] = m.ncols;
+  dims[2] = m.nnzb;
+  dims[3] = (int64_t)m.R * 1000 + m.C;
+  if (rowptr) TMG_CUDA(cudaMemcpyAsync(rowptr, m.rowptr.get(), (m.nrows + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (col) TMG_CUDA(cudaMemcpyAsync(col, m.col.get(), m.nnzb * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (val)
+    TMG_CUDA(cudaMemcpyAsync(val, m.val.get(), m.nnzb * m.R * m.C * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+}
+
+int tmg_hierarchy_export(tmg_hierarchy* h, int32_t level, int32_t what, int64_t* dims, int32_t* rowptr, int32_t* col,
+                         double* val, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h && dims, "hierarchy/dims is NULL");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  Level& l = *h->h->lv[level];
+  cudaStream_t s = S(stream);
+  switch (what) {
+    case 0: {  // level operator as BSR
+      if (l.lattice()) {
+        Bsr tmp;
+        if (h->h->dim == 2) lattice_to_bsr<2>(l, tmp, s);
+        else lattice_to_bsr<3>(l, tmp, s);
+        copy_bsr(tmp, dims, rowptr, col, val, s);
+      } else {
+        copy_bsr(l.Ab, dims, rowptr, col, val, s);
+      }
+      break;
+    }
+    case 1:
+      TMG_REQUIRE(l.xfer == XF_SPARSE, "level has no algebraic prolongation");
+      copy_bsr(l.P, dims, rowptr, col, val, s);
+      break;
+    case 4:
+      TMG_REQUIRE(l.xfer == XF_SPARSE, "level has no tentative prolongation");
+      copy_bsr(l.Tm, dims, rowptr, col, val, s);
+      break;
+    case 2: {  // strength graph
+      TMG_REQUIRE(l.xfer == XF_SPARSE, "level has no strength graph");
+      const int n = (int)(l.ndof / l.bs);
+      int nnz = 0;
+      TMG_CUDA(cudaMemcpyAsync(&nnz, l.sptr.get() + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TMG_CUDA(cudaStreamSynchronize(s));
+      dims[0] = n; dims[1] = n; dims[2] = nnz; dims[3] = 0;
+      if (rowptr) TMG_CUDA(cudaMemcpyAsync(rowptr, l.sptr.get(), (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (col && nnz) TMG_CUDA(cudaMemcpyAsync(col, l.scol.get(), nnz * sizeof(int), cudaMemcpyDeviceToHost, s));
+      TMG_CUDA(cudaStreamSynchronize(s));
+      break;
+    }
+    case 3: {  // aggregates
+      TMG_REQUIRE(l.xfer == XF_SPARSE, "level has no aggregates");
+      const int n = (int)(l.ndof / l.bs);
+      dims[0] = n; dims[1] = l.n_agg; dims[2] = n; dims[3] = 0;
+      if (col) TMG_CUDA(cudaMemcpyAsync(col, l.agg.get(), n * sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (val) TMG_CUDA(cudaMemcpyAsync(val, l.rho.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+      TMG_CUDA(cudaStreamSynchronize(s));
+      break;
+    }
+    default:
+      throw Error(TMG_EINVAL, "unknown export kind");
   }
   ABI_END
 }
@@ -310,8 +444,8 @@ int tmg_hierarchy_level_apply(tmg_hierarchy* h, int32_t level, const double* x, 
   ABI_BEGIN
   TMG_REQUIRE(h, "hierarchy is NULL");
   if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
-  if (h->h->dim == 2) level_apply<2>(*h->h->lv[level], x, y, S(stream));
-  else level_apply<3>(*h->h->lv[level], x, y, S(stream));
+  if (h->h->dim == 2) lvl_apply<2>(*h->h->lv[level], x, y, S(stream));
+  else lvl_apply<3>(*h->h->lv[level], x, y, S(stream));
   TMG_CUDA(cudaGetLastError());
   ABI_END
 }
@@ -341,18 +475,14 @@ int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, d
     constexpr int DIM = decltype(dimtag)::value;
     Hierarchy& H = *h->h;
     Level& l = *H.lv[level];
-    with_op<DIM>(l, [&](auto o) {
-      for (int r = 0; r < reps + 1; ++r) {
-        if (r == 1) TMG_CUDA(cudaEventRecord(a, s));
-        if (H.sm.kind == SM_CHEBYSHEV)
-          k_cheb<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, l.r.get(), l.p.get(), l.dinv.get(), l.coef.get(), 1, 0,
-                                                               l.x.get(), l.pt.get(), l.rt.get());
-        else
-          k_jacobi<DIM, decltype(o), false><<<TMG_NODE_LAUNCH(l), s>>>(o, l.x.get(), l.b.get(), l.dinv.get(),
-                                                                       l.wdev.get(), l.xt.get(),
-                                                                       Red{nullptr, nullptr, nullptr});
-      }
-    });
+    const Red nored{nullptr, nullptr, nullptr};
+    for (int r = 0; r < reps + 1; ++r) {
+      if (r == 1) TMG_CUDA(cudaEventRecord(a, s));
+      if (H.sm.kind == SM_CHEBYSHEV)
+        lvl_cheb_step<DIM>(l, l.r.get(), l.p.get(), 1, false, l.x.get(), l.pt.get(), l.rt.get(), s);
+      else
+        lvl_sweep<DIM, false>(H, l, l.b.get(), l.x.get(), l.xt.get(), nored, s);
+    }
   };
   if (h->h->dim == 2) run(std::integral_constant<int, 2>());
   else run(std::integral_constant<int, 3>());

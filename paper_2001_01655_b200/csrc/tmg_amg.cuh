@@ -1,0 +1,622 @@
+// Smoothed-aggregation AMG setup on the device (reference multigrid.py:343-566).
+//
+//  strength_of_connection (multigrid.py:355)  -> k_strength_*   (exact op order,
+//       no FMA contraction, so the kept/dropped decision matches scipy's)
+//  aggregate_nodes (multigrid.py:380)         -> exact parallel reproduction of the
+//       sequential greedy passes:
+//       pass 1 roots = lexicographically-first maximal independent set of the
+//       distance-2 graph (a node becomes a root iff no lower-numbered root is
+//       within two strong edges) -- computed in rounds by a cooperative kernel;
+//       pass-1 members join their (unique) adjacent root; pass-2 leftovers take
+//       the aggregate of their lowest-numbered neighbour that is aggregated at
+//       that point of the sequential sweep (pass-1 members or earlier leftovers),
+//       resolved by following those pointers; isolated nodes become singletons.
+//  _merge_small_aggregates (multigrid.py:427) -> fast path for the only case the
+//       configs produce (min_size 2: small = isolated singletons, which all fold
+//       into the last regular aggregate) and an exact sequential kernel otherwise.
+//  tentative_prolongation (multigrid.py:471)  -> one CTA per aggregate, LAPACK
+//       dgeqr2/dorg2r Householder conventions (numpy.linalg.qr).
+//  estimate_spectral_radius / smoothed_prolongation (multigrid.py:504-525)
+//  Galerkin P^T A P (multigrid.py:262)        -> BSR SpGEMM, deterministic order.
+#pragma once
+#include <cooperative_groups.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "tmg_bsr.cuh"
+
+namespace tmg {
+
+namespace cg = cooperative_groups;
+
+// ----------------------------------------------------------------------------
+// lattice operator (FineOp / StencilOp) -> BSR with its 3^DIM neighbour blocks
+// ----------------------------------------------------------------------------
+template <int DIM, class Op>
+__global__ void k_lattice_bsr_count(const __grid_constant__ Op op, int* __restrict__ cnt) {
+  TMG_NODE_IDX
+  if (!active) return;
+  int c = 0;
+#pragma unroll
+  for (int s = 0; s < Slots<DIM>::NS; ++s)
+    c += op.L.inside(ci + Slots<DIM>::dx(s), cj + Slots<DIM>::dy(s), ck + Slots<DIM>::dz(s)) ? 1 : 0;
+  cnt[node] = c;
+}
+template <int DIM, class Op>
+__global__ void k_lattice_bsr_fill(const __grid_constant__ Op op, const int* __restrict__ rowptr,
+                                   int* __restrict__ col, double* __restrict__ val) {
+  TMG_NODE_IDX
+  if (!active) return;
+  int p = rowptr[node];
+  for (int s = 0; s < Slots<DIM>::NS; ++s) {  // slot order == ascending node id
+    const int ii = ci + Slots<DIM>::dx(s), jj = cj + Slots<DIM>::dy(s), kk = ck + Slots<DIM>::dz(s);
+    if (!op.L.inside(ii, jj, kk)) continue;
+    double blk[DIM * DIM];
+    op.block(ci, cj, ck, ii, jj, kk, blk);
+    col[p] = op.L.id(ii, jj, kk);
+    for (int q = 0; q < DIM * DIM; ++q) val[(long long)p * DIM * DIM + q] = blk[q];
+    ++p;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// strength of connection: M_IJ = ||A_IJ||_F^2 in scipy's (R @ K.*K @ R^T) order
+// ----------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ double block_sq(const double* __restrict__ blk) {
+  double m = 0.0;
+#pragma unroll
+  for (int b = 0; b < R; ++b) {
+    double xb = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) xb = __dadd_rn(xb, __dmul_rn(blk[a * R + b], blk[a * R + b]));
+    m = __dadd_rn(m, xb);
+  }
+  return m;
+}
+template <int R>
+__global__ void k_strength_diag(BsrView<R, R> A, double* __restrict__ md, unsigned* __restrict__ bad) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.nrows) return;
+  double m = 0.0;
+  for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p)
+    if (A.col[p] == row) m = block_sq<R>(A.val + (long long)p * R * R);
+  md[row] = m;
+  if (m == 0.0) atomicOr(bad, 1u);
+}
+template <int R, bool FILL>
+__global__ void k_strength(BsrView<R, R> A, const double* __restrict__ md, double beta, int* __restrict__ cnt,
+                           const int* __restrict__ sptr, int* __restrict__ scol) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.nrows) return;
+  int c = 0;
+  int q = FILL ? sptr[row] : 0;
+  const double mi = md[row];
+  for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {
+    const int j = A.col[p];
+    if (j == row) continue;
+    const double m = block_sq<R>(A.val + (long long)p * R * R);
+    if (m > __dmul_rn(beta, __dsqrt_rn(__dmul_rn(mi, md[j])))) {
+      if (FILL) scol[q++] = j;
+      else ++c;
+    }
+  }
+  if (!FILL) cnt[row] = c;
+}
+
+// ----------------------------------------------------------------------------
+// aggregation
+// ----------------------------------------------------------------------------
+enum : int { ST_UND = 0, ST_ROOT = 1, ST_MEMBER = 2, ST_ISO = 3 };
+
+__global__ void k_agg_init(const int* __restrict__ sptr, int n, int* __restrict__ st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) st[i] = (sptr[i + 1] == sptr[i]) ? ST_ISO : ST_UND;
+}
+
+// Rounds of the distance-2 LFMIS in one cooperative launch.  Decisions are final
+// and monotone, so reading neighbours' states while they are being written only
+// changes WHEN a node decides, never WHAT it decides.
+__global__ void k_lfmis(const int* __restrict__ sptr, const int* __restrict__ scol, int n, int* st,
+                        int* __restrict__ last_undecided_round, int* __restrict__ rounds_out) {
+  cg::grid_group grid = cg::this_grid();
+  volatile int* vst = st;
+  const int stride = gridDim.x * blockDim.x;
+  for (int round = 1;; ++round) {
+    bool pending = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      if (vst[i] != ST_UND) continue;
+      bool root_near = false, und_near = false;
+      for (int p = sptr[i]; p < sptr[i + 1] && !root_near; ++p) {
+        const int j = scol[p];
+        if (j < i) {
+          const int s = vst[j];
+          root_near |= s == ST_ROOT;
+          und_near |= s == ST_UND;
+        }
+        for (int q = sptr[j]; q < sptr[j + 1]; ++q) {
+          const int k = scol[q];
+          if (k >= i) break;  // sorted: only lower-numbered nodes matter
+          const int s = vst[k];
+          root_near |= s == ST_ROOT;
+          und_near |= s == ST_UND;
+        }
+      }
+      if (root_near) vst[i] = ST_MEMBER;
+      else if (!und_near) vst[i] = ST_ROOT;
+      else pending = true;
+    }
+    if (pending) atomicMax(last_undecided_round, round);
+    grid.sync();
+    if (*(volatile int*)last_undecided_round < round) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *rounds_out = round;
+      return;
+    }
+  }
+}
+
+// pass-1 aggregate ids: roots by rank; members by their adjacent root; -1 isolated; -2 leftover
+__global__ void k_agg_pass1(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
+                            const int* __restrict__ st, const int* __restrict__ rank, int* __restrict__ agg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = st[i];
+  if (s == ST_ROOT) { agg[i] = rank[i]; return; }
+  if (s == ST_ISO) { agg[i] = -1; return; }
+  int a = -2;
+  for (int p = sptr[i]; p < sptr[i + 1]; ++p)
+    if (st[scol[p]] == ST_ROOT) { a = rank[scol[p]]; break; }
+  agg[i] = a;
+}
+// pass 2 pointer: lowest neighbour aggregated by pass 1, or a lower-numbered leftover
+__global__ void k_agg_pass2_ptr(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
+                                const int* __restrict__ agg1, int* __restrict__ ptr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int t = -1;
+  if (agg1[i] == -2)
+    for (int p = sptr[i]; p < sptr[i + 1]; ++p) {
+      const int j = scol[p];
+      if (agg1[j] >= 0 || (agg1[j] == -2 && j < i)) { t = j; break; }
+    }
+  ptr[i] = t;
+}
+__global__ void k_agg_pass2_resolve(int n, const int* __restrict__ agg1, const int* __restrict__ ptr,
+                                    int* __restrict__ agg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int a = agg1[i];
+  if (a == -2) {
+    int t = ptr[i];
+    while (t >= 0 && agg1[t] == -2) t = ptr[t];
+    a = t >= 0 ? agg1[t] : -1;
+  }
+  agg[i] = a;
+}
+__global__ void k_flag_eq(const int* __restrict__ v, int n, int val, int* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v[i] == val ? 1 : 0;
+}
+__global__ void k_assign_isolated(int n, const int* __restrict__ rank_iso, int base, int* __restrict__ agg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && agg[i] == -1) agg[i] = base + rank_iso[i];
+}
+__global__ void k_fill_value_where(int* __restrict__ agg, int n, int from, int to) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && agg[i] == from) agg[i] = to;
+}
+__global__ void k_pairwise(int* __restrict__ agg, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) agg[i] = i / 2;
+}
+__global__ void k_histogram(const int* __restrict__ agg, int n, int* __restrict__ size) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(size + agg[i], 1);
+}
+
+// Exact sequential _merge_small_aggregates (multigrid.py:427-468) for the general
+// case (min_size > 2 or forced-pairwise leftovers).  One thread; used rarely.
+__global__ void k_merge_small_seq(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
+                                  int* __restrict__ agg, int* __restrict__ size, int n_agg, int min_size,
+                                  int* __restrict__ remap, int* __restrict__ n_out) {
+  if (threadIdx.x || blockIdx.x) return;
+  // first loop over the originally-small aggregates, ascending
+  for (int a = 0; a < n_agg; ++a) {
+    if (size[a] >= min_size) continue;
+    // (size[a] may have changed since the np.flatnonzero(sizes < min_size) snapshot
+    //  only by growing through an earlier merge into a -- impossible: targets are
+    //  never small.  So the live test equals the snapshot test.)
+    int tgt = -1;
+    for (int i = 0; i < n && tgt < 0; ++i) {
+      if (agg[i] != a) continue;
+      for (int p = sptr[i]; p < sptr[i + 1]; ++p) {
+        const int j = scol[p];
+        if (agg[j] != a && size[agg[j]] >= min_size) { tgt = agg[j]; break; }
+      }
+    }
+    if (tgt >= 0) {
+      int moved = 0;
+      for (int i = 0; i < n; ++i)
+        if (agg[i] == a) { agg[i] = tgt; ++moved; }
+      size[tgt] += moved;
+      size[a] = 0;
+    }
+  }
+  // np.unique(return_inverse) renumbering + fallback folding into index neighbours
+  while (true) {
+    for (int a = 0; a < n_agg; ++a) remap[a] = -1;
+    for (int i = 0; i < n; ++i) remap[agg[i]] = 1;
+    int m = 0;
+    for (int a = 0; a < n_agg; ++a)
+      if (remap[a] == 1) remap[a] = m++;
+    for (int a = 0; a < n_agg; ++a) size[a] = 0;
+    for (int i = 0; i < n; ++i) { agg[i] = remap[agg[i]]; size[agg[i]]++; }
+    n_agg = m;
+    if (m < 2) break;
+    int small = -1;
+    for (int a = 0; a < m; ++a)
+      if (size[a] < min_size) { small = a; break; }
+    if (small < 0) break;
+    const int tgt = small > 0 ? small - 1 : small + 1;
+    for (int i = 0; i < n; ++i)
+      if (agg[i] == small) agg[i] = tgt;
+  }
+  *n_out = n_agg;
+}
+
+// ----------------------------------------------------------------------------
+// tentative prolongation: per-aggregate Householder QR (LAPACK dgeqr2 + dorg2r)
+// ----------------------------------------------------------------------------
+__device__ double block_reduce_sum(double v, double* sh) {
+  // blockDim.x <= 1024, multiple of 32
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+// dnrm2 with the classic scaled sum of squares (LAPACK <= 3.9 reference algorithm)
+__device__ double block_nrm2(const double* x, int m, double* sh) {
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, fabs(x[i]));
+  // block max
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_down_sync(0xffffffffu, t, o));
+    if (threadIdx.x == 0) sh[33] = t;
+  }
+  __syncthreads();
+  const double scale = sh[33];
+  if (scale == 0.0) return 0.0;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double q = x[i] / scale;
+    s += q * q;
+  }
+  s = block_reduce_sum(s, sh);
+  return scale * sqrt(s);
+}
+
+// One CTA per aggregate.  A: column-major m x nv working copy (global scratch).
+__global__ void k_tentative_qr(const int* __restrict__ offs, const int* __restrict__ members, int bs, int nv,
+                               const double* __restrict__ B, double* __restrict__ work, const long long* woff,
+                               double* __restrict__ Tval, double* __restrict__ Bc, int* __restrict__ bad) {
+  __shared__ double sh[40];
+  __shared__ double tau[8];
+  const int a = blockIdx.x;
+  const int n0 = offs[a], cnt = offs[a + 1] - n0;
+  const int m = cnt * bs;
+  if (m < nv) {
+    if (threadIdx.x == 0) atomicMax(bad, m > 0 ? m : 1);
+    return;
+  }
+  double* A = work + woff[a];  // column-major, lda = m
+  for (int t = threadIdx.x; t < m * nv; t += blockDim.x) {
+    const int r = t % m, c = t / m;
+    const int node = members[n0 + r / bs];
+    A[(long long)c * m + r] = B[((long long)node * bs + r % bs) * nv + c];
+  }
+  __syncthreads();
+  // dgeqr2
+  for (int k = 0; k < nv; ++k) {
+    double* col = A + (long long)k * m;
+    const double alpha = col[k];
+    const double xnorm = block_nrm2(col + k + 1, m - k - 1, sh);
+    double tk = 0.0, beta = alpha;
+    if (xnorm != 0.0) {
+      const double h = hypot(alpha, xnorm);
+      beta = signbit(alpha) ? h : -h;  // -SIGN(dlapy2, alpha), IEEE sign of alpha
+      tk = (beta - alpha) / beta;
+      const double sc = 1.0 / (alpha - beta);
+      for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) col[i] *= sc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tau[k] = tk;
+      col[k] = beta;
+    }
+    __syncthreads();
+    if (tk != 0.0) {
+      for (int j = k + 1; j < nv; ++j) {  // dlarf: A(k:m, j) -= tau v (v^T A(k:m, j))
+        double* cj = A + (long long)j * m;
+        double w = 0.0;
+        for (int i = k + threadIdx.x; i < m; i += blockDim.x) w += (i == k ? 1.0 : col[i]) * cj[i];
+        w = block_reduce_sum(w, sh);
+        for (int i = k + threadIdx.x; i < m; i += blockDim.x) cj[i] -= tk * w * (i == k ? 1.0 : col[i]);
+        __syncthreads();
+      }
+    }
+  }
+  // R -> Bc (nv x nv block of the coarse candidates)
+  for (int t = threadIdx.x; t < nv * nv; t += blockDim.x) {
+    const int r = t / nv, c = t % nv;
+    Bc[((long long)a * nv + r) * nv + c] = r <= c ? A[(long long)c * m + r] : 0.0;
+  }
+  __syncthreads();
+  // dorg2r: form Q in place (columns 0..nv-1)
+  for (int k = nv - 1; k >= 0; --k) {
+    double* col = A + (long long)k * m;
+    const double tk = tau[k];
+    if (k < nv - 1) {
+      if (threadIdx.x == 0) col[k] = 1.0;
+      __syncthreads();
+      for (int j = k + 1; j < nv; ++j) {
+        double* cj = A + (long long)j * m;
+        double w = 0.0;
+        for (int i = k + threadIdx.x; i < m; i += blockDim.x) w += col[i] * cj[i];
+        w = block_reduce_sum(w, sh);
+        for (int i = k + threadIdx.x; i < m; i += blockDim.x) cj[i] -= tk * w * col[i];
+        __syncthreads();
+      }
+    }
+    for (int i = k + 1 + threadIdx.x; i < m; i += blockDim.x) col[i] *= -tk;
+    __syncthreads();
+    if (threadIdx.x == 0) col[k] = 1.0 - tk;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) col[i] = 0.0;
+    __syncthreads();
+  }
+  // scatter Q rows into the node blocks of T (bs x nv per node)
+  for (int t = threadIdx.x; t < m * nv; t += blockDim.x) {
+    const int r = t % m, c = t / m;
+    const int node = members[n0 + r / bs];
+    Tval[((long long)node * bs + r % bs) * nv + c] = A[(long long)c * m + r];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// smoothed prolongation P = T - (omega D^-1) A T   (multigrid.py:518)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int sorted_unique_insert(int* list, int len, int v) {
+  int p = 0;
+  while (p < len && list[p] < v) ++p;
+  if (p < len && list[p] == v) return len;
+  for (int q = len; q > p; --q) list[q] = list[q - 1];
+  list[p] = v;
+  return len + 1;
+}
+constexpr int SP_MAXC = 64;  // distinct aggregates touched by one block row of A
+
+template <int BS, int NV, bool FILL>
+__global__ void k_smooth_p(BsrView<BS, BS> A, const int* __restrict__ agg, const double* __restrict__ Tval,
+                           const double* __restrict__ dinv, const double* __restrict__ rho, int* __restrict__ cnt,
+                           const int* __restrict__ prow, int* __restrict__ pcol, double* __restrict__ pval,
+                           int* __restrict__ overflow) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.nrows) return;
+  int cols[SP_MAXC];
+  int nc = 0;
+  nc = sorted_unique_insert(cols, nc, agg[row]);
+  for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {
+    if (nc >= SP_MAXC) { atomicOr(overflow, 1); return; }
+    nc = sorted_unique_insert(cols, nc, agg[A.col[p]]);
+  }
+  if (!FILL) { cnt[row] = nc; return; }
+  const double omega = 4.0 / (3.0 * fmax(*rho, 1e-30));
+  double dscale[BS];
+#pragma unroll
+  for (int r = 0; r < BS; ++r) dscale[r] = __dmul_rn(omega, dinv[(long long)row * BS + r]);
+  const int base = prow[row];
+  for (int q = 0; q < nc; ++q) {
+    const int J = cols[q];
+    double S[BS][NV];
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) S[r][c] = 0.0;
+    for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {
+      const int j = A.col[p];
+      if (agg[j] != J) continue;
+      const double* a = A.val + (long long)p * BS * BS;
+      const double* t = Tval + (long long)j * BS * NV;
+#pragma unroll
+      for (int r = 0; r < BS; ++r)
+#pragma unroll
+        for (int b = 0; b < BS; ++b)
+#pragma unroll
+          for (int c = 0; c < NV; ++c) S[r][c] = __dadd_rn(S[r][c], __dmul_rn(a[r * BS + b], t[b * NV + c]));
+    }
+    pcol[base + q] = J;
+    double* out = pval + (long long)(base + q) * BS * NV;
+    const bool own = J == agg[row];
+    const double* tr = Tval + (long long)row * BS * NV;
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        const double x = __dmul_rn(dscale[r], S[r][c]);
+        out[r * NV + c] = own ? __dsub_rn(tr[r * NV + c], x) : -x;
+      }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// BSR transpose and SpGEMM
+// ----------------------------------------------------------------------------
+__global__ void k_row_of(const int* __restrict__ rowptr, int nrows, int* __restrict__ rowof) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) rowof[p] = r;
+}
+__global__ void k_iota(int* __restrict__ v, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int)i;
+}
+__global__ void k_count_cols(const int* __restrict__ col, long long nnz, int* __restrict__ cnt) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p < nnz) atomicAdd(cnt + col[p], 1);
+}
+// Pt block q (sorted by column, then row) = transpose of P block perm[q]
+__global__ void k_transpose_fill(const int* __restrict__ perm, const int* __restrict__ rowof,
+                                 const double* __restrict__ pval, int R, int C, long long nnz,
+                                 int* __restrict__ tcol, double* __restrict__ tval) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= nnz) return;
+  const int p = perm[q];
+  tcol[q] = rowof[p];
+  for (int a = 0; a < R; ++a)
+    for (int b = 0; b < C; ++b) tval[q * R * C + b * R + a] = pval[(long long)p * R * C + a * C + b];
+}
+
+// Symbolic SpGEMM: number of distinct column blocks in row i of X*Y.  One warp per
+// row with a shared-memory open-addressing set.
+constexpr int SG_WARPS = 4, SG_SLOTS = 1024;
+__global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __restrict__ xp, const int* __restrict__ xc,
+                                                                 const int* __restrict__ yp, const int* __restrict__ yc,
+                                                                 int nrows, int* __restrict__ cnt,
+                                                                 int* __restrict__ overflow) {
+  __shared__ int set[SG_WARPS][SG_SLOTS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * SG_WARPS + w;
+  if (row >= nrows) return;
+  for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
+  __syncwarp();
+  int mine = 0;
+  for (int p = xp[row]; p < xp[row + 1]; ++p) {
+    const int k = xc[p];
+    for (int q = yp[k] + lane; q < yp[k + 1]; q += 32) {
+      const int j = yc[q];
+      unsigned h = ((unsigned)j * 2654435761u) & (SG_SLOTS - 1);
+      for (int probe = 0;; ++probe) {
+        if (probe == SG_SLOTS) { atomicOr(overflow, 1); break; }
+        const int prev = atomicCAS(&set[w][h], -1, j);
+        if (prev == -1) { ++mine; break; }
+        if (prev == j) break;
+        h = (h + 1) & (SG_SLOTS - 1);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+  if (lane == 0) cnt[row] = mine;
+}
+// Numeric SpGEMM: collect the row's distinct columns (sorted), then each output
+// block C_ij = sum_k X_ik Y_kj with k ascending (deterministic).
+template <int R1, int K1, int C2>
+__global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_fill(const int* __restrict__ xp, const int* __restrict__ xc,
+                                                                const double* __restrict__ xv,
+                                                                const int* __restrict__ yp, const int* __restrict__ yc,
+                                                                const double* __restrict__ yv, int nrows,
+                                                                const int* __restrict__ cp, int* __restrict__ cc,
+                                                                double* __restrict__ cv) {
+  __shared__ int set[SG_WARPS][SG_SLOTS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * SG_WARPS + w;
+  if (row >= nrows) return;
+  for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
+  __syncwarp();
+  for (int p = xp[row]; p < xp[row + 1]; ++p) {
+    const int k = xc[p];
+    for (int q = yp[k] + lane; q < yp[k + 1]; q += 32) {
+      const int j = yc[q];
+      unsigned h = ((unsigned)j * 2654435761u) & (SG_SLOTS - 1);
+      for (int probe = 0; probe < SG_SLOTS; ++probe) {
+        const int prev = atomicCAS(&set[w][h], -1, j);
+        if (prev == -1 || prev == j) break;
+        h = (h + 1) & (SG_SLOTS - 1);
+      }
+    }
+  }
+  __syncwarp();
+  const int base = cp[row];
+  // rank of every stored key = its sorted position
+  for (int s = lane; s < SG_SLOTS; s += 32) {
+    const int key = set[w][s];
+    if (key < 0) continue;
+    int rank = 0;
+    for (int t = 0; t < SG_SLOTS; ++t) {
+      const int o = set[w][t];
+      rank += (o >= 0 && o < key) ? 1 : 0;
+    }
+    cc[base + rank] = key;
+  }
+  __syncwarp();
+  const int nout = cp[row + 1] - base;
+  for (int o = lane; o < nout; o += 32) {
+    const int j = cc[base + o];
+    double acc[R1 * C2];
+#pragma unroll
+    for (int t = 0; t < R1 * C2; ++t) acc[t] = 0.0;
+    for (int p = xp[row]; p < xp[row + 1]; ++p) {
+      const int k = xc[p];
+      int lo = yp[k], hi = yp[k + 1] - 1, hit = -1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1, v = yc[mid];
+        if (v == j) { hit = mid; break; }
+        if (v < j) lo = mid + 1; else hi = mid - 1;
+      }
+      if (hit < 0) continue;
+      const double* X = xv + (long long)p * R1 * K1;
+      const double* Y = yv + (long long)hit * K1 * C2;
+#pragma unroll
+      for (int a = 0; a < R1; ++a)
+#pragma unroll
+        for (int b = 0; b < C2; ++b) {
+          double s = acc[a * C2 + b];
+#pragma unroll
+          for (int c = 0; c < K1; ++c) s += X[a * K1 + c] * Y[c * C2 + b];
+          acc[a * C2 + b] = s;
+        }
+    }
+    double* out = cv + (long long)(base + o) * R1 * C2;
+#pragma unroll
+    for (int t = 0; t < R1 * C2; ++t) out[t] = acc[t];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host helpers (stream-ordered; cub temporaries per call)
+// ----------------------------------------------------------------------------
+inline void exclusive_scan(const int* in, int* out, int n, cudaStream_t s) {
+  size_t tb = 0;
+  TMG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s));
+  DevBuf<char> tmp;
+  tmp.alloc(tb, s);
+  TMG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, in, out, n, s));
+}
+// rowptr (n+1) from counts: scan over n+1 entries with a trailing 0
+inline void rowptr_from_counts(DevBuf<int>& cnt_np1, DevBuf<int>& rowptr, int n, cudaStream_t s) {
+  rowptr.alloc(n + 1, s);
+  exclusive_scan(cnt_np1.get(), rowptr.get(), n + 1, s);
+}
+inline int read_int(const int* d, cudaStream_t s) {
+  int h = 0;
+  TMG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace tmg

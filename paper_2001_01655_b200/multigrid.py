@@ -135,6 +135,56 @@ class MgHierarchy:
         return [{"size": lv.size, "nonzeros": lv.nonzeros, "provenance": lv.provenance}
                 for lv in self.levels]
 
+    def device_flags(self):
+        buf = C.create_string_buffer(4096)
+        _lib.check(_lib.load().tmg_hierarchy_flags(self._h, buf, 4096))
+        s = buf.value.decode()
+        return s.split(",") if s else []
+
+    # -- parity exports (host copies of device data; tests only) --------------
+    def _export(self, k, what):
+        dims = (C.c_int64 * 4)()
+        L = _lib.load()
+        _lib.check(L.tmg_hierarchy_export(self._h, k, what, dims, None, None, None, stream_ptr(None)))
+        nr, nc, nnz, rc = (int(v) for v in dims)
+        rowptr = np.zeros(nr + 1, np.int32)
+        col = np.zeros(max(nnz, 1), np.int32)
+        R, Cc = (rc // 1000, rc % 1000) if rc else (0, 0)
+        val = np.zeros(max(nnz * R * Cc, 1))
+        _lib.check(L.tmg_hierarchy_export(self._h, k, what, dims, rowptr.ctypes.data, col.ctypes.data,
+                                          val.ctypes.data, stream_ptr(None)))
+        return nr, nc, nnz, R, Cc, rowptr, col[:nnz], val
+
+    def _bsr(self, k, what):
+        import scipy.sparse as sp
+        nr, nc, nnz, R, Cc, rowptr, col, val = self._export(k, what)
+        return sp.bsr_matrix((val[:nnz * R * Cc].reshape(nnz, R, Cc), col, rowptr),
+                             shape=(nr * R, nc * Cc)).tocsr()
+
+    def level_matrix(self, k):
+        return self._bsr(k, 0)
+
+    def prolongation(self, k):
+        return self._bsr(k, 1)
+
+    def tentative(self, k):
+        return self._bsr(k, 4)
+
+    def strength(self, k):
+        import scipy.sparse as sp
+        nr, nc, nnz, R, Cc, rowptr, col, val = self._export(k, 2)
+        return sp.csr_matrix((np.ones(nnz), col, rowptr), shape=(nr, nr))
+
+    def aggregates(self, k):
+        dims = (C.c_int64 * 4)()
+        L = _lib.load()
+        _lib.check(L.tmg_hierarchy_export(self._h, k, 3, dims, None, None, None, stream_ptr(None)))
+        agg = np.zeros(int(dims[0]), np.int32)
+        rho = np.zeros(1)
+        _lib.check(L.tmg_hierarchy_export(self._h, k, 3, dims, None, agg.ctypes.data, rho.ctypes.data,
+                                          stream_ptr(None)))
+        return agg.astype(np.int64), float(rho[0])
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._lib is not None:
@@ -175,3 +225,66 @@ def build_gmg(mesh, K, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, max_le
                                          C.byref(smoother.desc()), int(n_pre), int(n_post),
                                          stream_ptr(stream), C.byref(h)))
     return MgHierarchy(h, K, smoother, n_pre, n_post, flags)
+
+
+def _start_vector(n, seed):
+    """numpy default_rng(seed).standard_normal(n): the power-method start vector of
+    estimate_spectral_radius (multigrid.py:508-509); host-side input data."""
+    return np.ascontiguousarray(np.random.default_rng(seed).standard_normal(n))
+
+
+def build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0,
+                 beta=DEFAULT_STRENGTH_BETA, stream=None):
+    """Smoothed-aggregation hierarchy built on the device (multigrid.py:555).
+    EXTENSION: beta (the reference fixes 0.003)."""
+    smoother = smoother or SmootherConfig()
+    B = np.asarray(near_nullspace, dtype=float)
+    if B.ndim != 2 or B.shape[0] != K.shape[0]:
+        raise ValueError("near_nullspace must be (ndofs, nvec)")
+    if smoother.kind not in SMOOTHER_KINDS:
+        raise ValueError("unknown smoother kind %r" % smoother.kind)
+    B = np.ascontiguousarray(B)
+    v0 = _start_vector(K.shape[0], seed)
+    h = C.c_void_p()
+    _lib.check(_lib.load().tmg_sa_amg_build(K.handle, B.ctypes.data, B.shape[1], int(coarse_max_dofs),
+                                            float(beta), v0.ctypes.data, C.byref(smoother.desc()),
+                                            int(n_pre), int(n_post), stream_ptr(stream), C.byref(h)))
+    H = MgHierarchy(h, K, smoother, n_pre, n_post)
+    H.flags = H.device_flags()
+    return H
+
+
+def hybrid_plan(mesh, n_geo, coarse_max_dofs):
+    """Geometric part of build_hybrid (multigrid.py:589-601): (dims, sizes, flags)."""
+    dims, sizes, flags = mesh.dims, mesh.element_size, []
+    ndof = mesh.total_dofs
+    for _ in range(n_geo):
+        if all(d <= 1 for d in dims):
+            flags.append("geometric_coarsening_exhausted")
+            break
+        if ndof <= coarse_max_dofs:
+            break
+        dims = _coarsen_dims(dims)
+        sizes = tuple(2 * h for h in sizes)
+        ndof = mesh.dofs_per_node * int(np.prod([d + 1 for d in dims]))
+    return dims, sizes, flags
+
+
+def build_hybrid(mesh, K, near_nullspace, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_post=1,
+                 seed=0, beta=DEFAULT_STRENGTH_BETA, stream=None):
+    """Geometric transfers on the finest n_geo levels, SA below (multigrid.py:573)."""
+    from .mesh import StructuredMesh, rigid_body_modes
+    smoother = smoother or SmootherConfig()
+    if n_geo <= 0:
+        return build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother, n_pre, n_post, seed, beta, stream)
+    dims, sizes, _ = hybrid_plan(mesh, n_geo, coarse_max_dofs)
+    Bc = np.ascontiguousarray(rigid_body_modes(StructuredMesh(dims, sizes)))
+    v0 = _start_vector(Bc.shape[0], seed)
+    h = C.c_void_p()
+    _lib.check(_lib.load().tmg_hybrid_build(K.handle, int(n_geo), Bc.ctypes.data, Bc.shape[0], Bc.shape[1],
+                                            int(coarse_max_dofs), float(beta), v0.ctypes.data,
+                                            C.byref(smoother.desc()), int(n_pre), int(n_post),
+                                            stream_ptr(stream), C.byref(h)))
+    H = MgHierarchy(h, K, smoother, n_pre, n_post)
+    H.flags = H.device_flags()
+    return H

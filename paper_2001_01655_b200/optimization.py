@@ -11,8 +11,8 @@ import numpy as np
 
 from . import _lib, krylov
 from ._dev import as_dev, empty_dev, ptr, stream_ptr
-from .mesh import assemble_stiffness
-from .multigrid import SmootherConfig, build_gmg
+from .mesh import assemble_stiffness, rigid_body_modes
+from .multigrid import DEFAULT_STRENGTH_BETA, SmootherConfig, build_gmg, build_hybrid, build_sa_amg
 
 
 @dataclass
@@ -32,6 +32,11 @@ class SolverHarness:
     n_pre: int = 1
     n_post: int = 1
     max_levels: int | None = None
+    beta: float = DEFAULT_STRENGTH_BETA
+
+    @property
+    def near_nullspace(self):
+        return rigid_body_modes(self.mesh, self.fixed_dofs)
 
     def build(self, K):
         torch_sync()
@@ -41,6 +46,12 @@ class SolverHarness:
         if self.strategy == "gmg":
             h = build_gmg(self.mesh, K, self.coarse_max_dofs, self.smoother, self.n_pre, self.n_post,
                           self.max_levels)
+        elif self.strategy == "amg":
+            h = build_sa_amg(K, self.near_nullspace, self.coarse_max_dofs, self.smoother, self.n_pre,
+                             self.n_post, seed=self.seed, beta=self.beta)
+        elif self.strategy == "hybrid":
+            h = build_hybrid(self.mesh, K, self.near_nullspace, self.n_geo, self.coarse_max_dofs,
+                             self.smoother, self.n_pre, self.n_post, seed=self.seed, beta=self.beta)
         else:
             raise ValueError("unknown preconditioner strategy %r" % self.strategy)
         torch_sync()
