@@ -2,16 +2,17 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl b200|reference]
 
-A step is one drop-in call of the hot path on the config's workload: element
-moduli from rho, K(rho), hierarchy build, PCG to rtol=1e-8, compliance and
-sensitivity -- what one topology-optimisation iteration costs (the reference
-rebuilds the preconditioner every iteration, optimization.py:498 design note).
+A step is one drop-in call of the hot path on the config's workload, for every
+solver leg the config names (config 1: GMG 5 levels AND SA-AMG on identical
+inputs): element moduli from rho, K(rho), hierarchy build, PCG to rtol=1e-8,
+compliance and sensitivity -- what one topology-optimisation iteration costs
+(the reference rebuilds the preconditioner every iteration).
 Metric: DOF*iterations/s (higher is better) = sum(ndof*iters) / sum(step time).
 Inputs are resident in HBM when the timed region starts; L2 is flushed before
 every timed step.  ``e2e`` repeats the metric through the C-ABI host-buffer entry
 point (tmg_solve_compliance_host) with H2D/D2H copies inside the timed region.
 ``--impl reference`` times the CPU oracle port of the reference algorithm on a
-bounded sample (setup + a fixed number of PCG iterations) on rank 0.
+bounded sample (setup + a fixed number of PCG iterations per leg) on rank 0.
 Under torchrun every rank runs an independent replica (scaling: weak).
 """
 
@@ -52,13 +53,10 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def gmg_legs(w):
-    return [s for s in w.solvers if s["strategy"] == "gmg"]
-
-
-def config_dict(w, args, world, legs, pending):
+def config_dict(w, args, world):
+    from paper_2001_01655_b200 import problems
     return {"workload": w.name, "config_index": args.config, "ndof": int(w.ndof),
-            "elements": int(w.mesh.element_count), "legs": legs, "pending_legs": pending,
+            "elements": int(w.mesh.element_count), "legs": [problems.leg_name(s) for s in w.solvers],
             "rtol": w.rtol, "precision": "fp64", "l2": "flushed (256 MiB write) before every timed step",
             "parallelism": "replicas x%d" % world}
 
@@ -127,7 +125,14 @@ def oracle_sample(w, leg, iters):
         sm = O.Smoother("chebyshev", 1.0, leg.get("degree", 2))
     else:
         sm = O.Smoother(leg["smoother"], leg.get("weight", 0.5), safeguard=leg.get("safeguard", 0.0))
-    h = O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+    if leg["strategy"] == "gmg":
+        h = O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+    elif leg["strategy"] == "amg":
+        h = O.build_sa_amg(K, O.rigid_body_modes(g, w.bc.fixed_dofs), leg["coarse_max_dofs"], sm, leg["n_pre"],
+                           leg["n_post"], beta=leg["beta"])
+    else:
+        h = O.build_hybrid(g, K, O.rigid_body_modes(g, w.bc.fixed_dofs), leg["n_geo"], leg["coarse_max_dofs"], sm,
+                           leg["n_pre"], leg["n_post"], beta=leg["beta"])
     u, rec = O.pcg(K, w.bc.load_vector, None, h.apply, rtol=w.rtol, max_iterations=iters)
     O.compliance_sensitivity(g, w.bc.load_vector, u, w.rho, problems.PENAL, problems.E0, problems.EMIN)
     dt = time.perf_counter() - t0
@@ -139,11 +144,10 @@ def run_reference(args, rank, world):
         return
     from paper_2001_01655_b200 import problems
     w = problems.CONFIGS[args.config]()
-    legs = gmg_legs(w)
     work = secs = 0.0
     for step in range(args.warmup + args.steps):
         wk = dt = 0.0
-        for leg in legs:
+        for leg in w.solvers:
             a, b, _ = oracle_sample(w, leg, args.cpu_sample_iters)
             wk += a
             dt += b
@@ -151,13 +155,13 @@ def run_reference(args, rank, world):
             work += wk
             secs += dt
     value = work / secs
-    sample = "oracle port: setup + %d PCG iterations per leg (%s) per step" % (
-        args.cpu_sample_iters, ",".join("gmg%d" % l["levels"] for l in legs))
+    sample = "oracle port (numpy/scipy, 1 thread): setup + %d PCG iterations per leg (%s) per step" % (
+        args.cpu_sample_iters, ",".join(problems.leg_name(l) for l in w.solvers))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
-            "config": config_dict(w, args, 1, ["gmg%d" % l["levels"] for l in legs], []),
+            "config": config_dict(w, args, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -166,6 +170,67 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+class LegRunner:
+    """Device-resident inputs and the drop-in call sequence of one solver leg."""
+
+    def __init__(self, w, leg):
+        import torch
+
+        import paper_2001_01655_b200 as T
+        from paper_2001_01655_b200 import problems
+        self.T, self.w, self.leg = T, w, leg
+        self.name = problems.leg_name(leg)
+        self.sm = problems.smoother_settings(leg)
+        self.maxit = leg.get("max_iterations", 10000)
+        if leg["strategy"] == "amg":
+            B = T.rigid_body_modes(w.mesh, w.bc.fixed_dofs)
+            self.B = torch.as_tensor(B, device="cuda")
+            self.v0 = torch.as_tensor(np.random.default_rng(0).standard_normal(w.ndof), device="cuda")
+        elif leg["strategy"] == "hybrid":
+            self.B = T.rigid_body_modes(w.mesh, w.bc.fixed_dofs)
+
+    def build(self, K):
+        T, w, leg = self.T, self.w, self.leg
+        if leg["strategy"] == "gmg":
+            return T.build_gmg(w.mesh, K, 1, self.sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+        if leg["strategy"] == "amg":
+            return T.build_sa_amg(K, self.B, leg["coarse_max_dofs"], self.sm, leg["n_pre"], leg["n_post"],
+                                  beta=leg["beta"], v0=self.v0)
+        return T.build_hybrid(w.mesh, K, self.B, leg["n_geo"], leg["coarse_max_dofs"], self.sm, leg["n_pre"],
+                              leg["n_post"], beta=leg["beta"])
+
+    def mg_desc(self):
+        """tmg_mg_desc for the host-buffer entry point (+ keep-alive host arrays)."""
+        from paper_2001_01655_b200 import _lib
+        from paper_2001_01655_b200.mesh import StructuredMesh, rigid_body_modes
+        from paper_2001_01655_b200.multigrid import hybrid_plan
+        leg, w = self.leg, self.w
+        mg = _lib.MgDesc()
+        mg.strategy = {"gmg": 0, "amg": 1, "hybrid": 2}[leg["strategy"]]
+        mg.coarse_max_dofs = leg.get("coarse_max_dofs", 1)
+        mg.max_levels = leg.get("levels", 0)
+        mg.smoother = self.sm.desc()
+        mg.n_pre, mg.n_post = leg["n_pre"], leg["n_post"]
+        keep = []
+        if leg["strategy"] == "amg":
+            B = np.ascontiguousarray(rigid_body_modes(w.mesh, w.bc.fixed_dofs))
+            v0 = np.random.default_rng(0).standard_normal(w.ndof)
+            keep = [B, v0]
+        elif leg["strategy"] == "hybrid":
+            dims, sizes, _ = hybrid_plan(w.mesh, leg["n_geo"], leg["coarse_max_dofs"])
+            B = np.ascontiguousarray(rigid_body_modes(StructuredMesh(dims, sizes)))
+            v0 = np.random.default_rng(0).standard_normal(B.shape[0])
+            keep = [B, v0]
+            mg.n_geo = leg["n_geo"]
+        if keep:
+            mg.beta = leg["beta"]
+            mg.near_nullspace_host = keep[0].ctypes.data
+            mg.nvec = keep[0].shape[1]
+            mg.coarse_ndof = keep[0].shape[0]
+            mg.v0_host = keep[1].ctypes.data
+        return mg, keep
+
+
 def run_b200(args, rank, world, local):
     import torch
 
@@ -178,42 +243,35 @@ def run_b200(args, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = problems.CONFIGS[args.config]()
-    legs = gmg_legs(w)
-    pending = [s["strategy"] for s in w.solvers if s["strategy"] != "gmg"]
+    runners = [LegRunner(w, leg) for leg in w.solvers]
     L = _lib.load()
     law = T.SimpLaw(penalty=problems.PENAL, e_min_ratio=problems.EMIN)
     rho_d = as_dev(w.rho)
     f_d = as_dev(w.bc.load_vector)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-
     state = {}
 
     def step():
         work = 0
-        iters = []
         state["legs"] = []
-        for leg in legs:
+        for lr in runners:
             E = law.modulus(rho_d)
             K = T.StiffnessOperator(w.mesh, w.bc, E)
-            sm = problems.gmg_settings(leg)
-            h = T.build_gmg(w.mesh, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
-            u, rec = T.cg_solve(K, f_d, None, h, T.SolveConfig(rtol=w.rtol,
-                                                              max_iterations=leg.get("max_iterations", 10000)))
+            h = lr.build(K)
+            u, rec = T.cg_solve(K, f_d, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=lr.maxit))
             dc = empty_dev(w.mesh.element_count)
             comp = C.c_double()
             _lib.check(L.tmg_compliance_sensitivity(K.handle, ptr(rho_d), ptr(f_d), ptr(u), law.penalty,
                                                     law.e_max, law.e_min, ptr(dc), C.byref(comp),
                                                     stream_ptr(None)))
             work += w.ndof * rec.iterations
-            iters.append(rec.iterations)
-            state["K"], state["h"], state["rec"], state["compliance"] = K, h, rec, comp.value
             hist = rec.residual_history
-            state["legs"].append({"leg": "%s%d" % (leg["strategy"], leg.get("levels", 0)),
-                                  "iterations": rec.iterations, "converged": rec.converged,
+            state["legs"].append({"leg": lr.name, "iterations": rec.iterations, "converged": rec.converged,
                                   "rel_residual": hist[-1] / hist[0], "solve_ms": rec.solve_time * 1e3,
-                                  "max_iterations": leg.get("max_iterations", 10000),
-                                  "compliance": comp.value})
-        return work, iters
+                                  "max_iterations": lr.maxit, "compliance": comp.value,
+                                  "levels": [lv.size for lv in h.levels]})
+            state.setdefault("h", h)
+        return work
 
     for _ in range(args.warmup):
         step()
@@ -221,19 +279,18 @@ def run_b200(args, rank, world, local):
     if world > 1:
         torch.distributed.barrier()
     launches0 = L.tmg_launch_count()
-    total_ms, total_work, it_log = 0.0, 0, []
+    total_ms, total_work = 0.0, 0
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            wk, its = step()
+            wk = step()
             e1.record()
             torch.cuda.synchronize()
             total_ms += e0.elapsed_time(e1)
             total_work += wk
-            it_log.append(its)
     launches = L.tmg_launch_count() - launches0
     if world > 1:
         torch.distributed.barrier()
@@ -241,25 +298,23 @@ def run_b200(args, rank, world, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = world * total_work / (total_ms / 1e3)
-
-    # dominant kernel: level-0 Jacobi sweep, timed live with CUDA events
     roof = roofline(args, w, state, L)
-
-    # end to end through the C-ABI host entry point
-    e2e = e2e_run(args, w, legs, L, law)
-
+    e2e = e2e_run(args, w, runners, L, law)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
-            "config": config_dict(w, args, world, ["gmg%d" % l["levels"] for l in legs], pending),
-            "pcg_iterations": it_log[-1], "leg_results": state["legs"],
+            "config": config_dict(w, args, world), "leg_results": state["legs"],
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        wk, dt, its = oracle_sample(w, legs[0], args.cpu_sample_iters)
+        wk = dt = 0.0
+        for leg in w.solvers:
+            a, b, _ = oracle_sample(w, leg, args.cpu_sample_iters)
+            wk += a
+            dt += b
         line["cpu_baseline"] = {"value": wk / dt, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": "oracle port (numpy/scipy, 1 thread): setup + %d PCG iterations "
-                                          "of the gmg%d leg, %.1f s" % (its, legs[0]["levels"], dt)}
+                                "sample": "oracle port (numpy/scipy, 1 thread): setup + %d PCG iterations of "
+                                          "each leg, %.1f s" % (args.cpu_sample_iters, dt)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -268,8 +323,6 @@ def run_b200(args, rank, world, local):
 
 def roofline(args, w, state, L):
     import torch
-
-    from paper_2001_01655_b200._dev import ptr
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -278,10 +331,8 @@ def roofline(args, w, state, L):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     h = state["h"]
     ms = C.c_double()
-    reps = 50
-    _lib_check = __import__("paper_2001_01655_b200._lib", fromlist=["check"]).check
-    _lib_check(L.tmg_hierarchy_time_smoother(h.handle, 0, reps, C.byref(ms),
-                                             torch.cuda.current_stream().cuda_stream))
+    from paper_2001_01655_b200._lib import check
+    check(L.tmg_hierarchy_time_smoother(h.handle, 0, 50, C.byref(ms), torch.cuda.current_stream().cuda_stream))
     mesh = w.mesh
     d = mesh.ndim
     nodes, nel = mesh.node_count, mesh.element_count
@@ -297,21 +348,12 @@ def roofline(args, w, state, L):
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "bytes_per_launch": bytes_launch, "launch_us": ms.value * 1e3,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-            "note": "working set %.1f MB (< 126 MB L2): the sweep can be L2-resident inside the solve"
-                    % (bytes_launch / 1e6)}
+            "timing": "CUDA events around 50 back-to-back launches on the launching stream",
+            "note": "working set %.1f MB vs 126 MB L2" % (bytes_launch / 1e6)}
 
 
-def e2e_run(args, w, legs, L, law):
+def e2e_run(args, w, runners, L, law):
     from paper_2001_01655_b200 import _lib
-    leg = legs[0]
-    sm = leg_desc(leg)
-    mg = _lib.MgDesc()
-    mg.strategy = 0
-    mg.coarse_max_dofs = 1
-    mg.max_levels = leg["levels"]
-    mg.smoother = sm
-    mg.n_pre, mg.n_post = leg["n_pre"], leg["n_post"]
-    cfg = _lib.SolveDesc(w.rtol, leg.get("max_iterations", 10000))
     rho = np.ascontiguousarray(w.rho, dtype=np.float64)
     f = np.ascontiguousarray(w.bc.load_vector)
     fixed = np.ascontiguousarray(w.bc.fixed_dofs, dtype=np.int64)
@@ -320,29 +362,30 @@ def e2e_run(args, w, legs, L, law):
     comp = C.c_double()
     rec = _lib.SolveRec()
     md = _lib.mesh_desc(w.mesh)
+    descs = [lr.mg_desc() for lr in runners]
+    cfgs = [_lib.SolveDesc(w.rtol, lr.maxit) for lr in runners]
 
     def call():
-        _lib.check(L.tmg_solve_compliance_host(C.byref(md), rho.ctypes.data, fixed.ctypes.data, fixed.size,
-                                               f.ctypes.data, law.penalty, law.e_max, law.e_min, 0.3,
-                                               C.byref(mg), C.byref(cfg), u.ctypes.data, dc.ctypes.data,
-                                               C.byref(comp), C.byref(rec)))
+        work = 0
+        for (mg, keep), cfg in zip(descs, cfgs):
+            _lib.check(L.tmg_solve_compliance_host(C.byref(md), rho.ctypes.data, fixed.ctypes.data, fixed.size,
+                                                   f.ctypes.data, law.penalty, law.e_max, law.e_min, 0.3,
+                                                   C.byref(mg), C.byref(cfg), u.ctypes.data, dc.ctypes.data,
+                                                   C.byref(comp), C.byref(rec)))
+            work += w.ndof * rec.iterations
+        return work
     call()
     work = secs = 0.0
     for _ in range(max(1, args.e2e_steps)):
         t0 = time.perf_counter()
-        call()
+        work += call()
         secs += time.perf_counter() - t0
-        work += w.ndof * rec.iterations
-    h2d = rho.nbytes + f.nbytes + w.mesh.node_count + 8 * (24 * 24)
-    d2h = u.nbytes + dc.nbytes + 8 + 8
+    h2d = sum(rho.nbytes + f.nbytes + w.mesh.node_count + 8 * 24 * 24 +
+              sum(a.nbytes for a in keep) for (mg, keep) in descs)
+    d2h = len(descs) * (u.nbytes + dc.nbytes + 16)
     return {"value": work / secs, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "leg": "gmg%d" % leg["levels"], "ms_per_step": 1e3 * secs / max(1, args.e2e_steps),
-            "timing": "host wall clock around tmg_solve_compliance_host (host buffers in/out)"}
-
-
-def leg_desc(leg):
-    from paper_2001_01655_b200 import problems
-    return problems.gmg_settings(leg).desc()
+            "ms_per_step": 1e3 * secs / max(1, args.e2e_steps),
+            "timing": "host wall clock around tmg_solve_compliance_host per leg (host buffers in/out)"}
 
 
 def main():

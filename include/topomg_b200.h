@@ -118,7 +118,8 @@ int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels,
  * n_post, seed).  near_nullspace_host: row-major (ndofs x nvec), nvec 3 (2D) or 6
  * (3D).  beta: strength threshold (reference: 0.003, multigrid.py:22).
  * v0_host: the power-method start vector numpy.random.default_rng(seed)
- * .standard_normal(ndofs) of multigrid.py:509 (deeper levels use its prefix). */
+ * .standard_normal(ndofs) of multigrid.py:509 (deeper levels use its prefix).
+ * Both arrays may be host or device pointers (copied with cudaMemcpyDefault). */
 int tmg_sa_amg_build(tmg_operator* K, const double* near_nullspace_host, int32_t nvec,
                      int64_t coarse_max_dofs, double beta, const double* v0_host,
                      const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
@@ -173,13 +174,19 @@ int tmg_compliance_sensitivity(tmg_operator* K, const double* rho_dev, const dou
 
 /* End-to-end drop-in for compliance_and_sensitivity (optimization.py:114) given the
  * filtered densities: HOST buffers in and out; H2D copies, modulus, operator,
- * hierarchy (GMG: strategy 0), PCG solve, sensitivity and D2H copies all inside. */
+ * hierarchy (gmg / amg / hybrid), PCG solve, sensitivity and D2H copies all inside. */
 typedef struct {
-  int32_t strategy;          /* 0 gmg */
+  int32_t strategy;          /* 0 gmg, 1 amg (smoothed aggregation), 2 hybrid */
   int64_t coarse_max_dofs;
-  int32_t max_levels;
+  int32_t max_levels;        /* gmg only; <= 0: no cap */
   tmg_smoother_desc smoother;
   int32_t n_pre, n_post;
+  int32_t n_geo;             /* hybrid */
+  double beta;               /* amg/hybrid strength threshold */
+  const double* near_nullspace_host;  /* amg: ndofs x nvec; hybrid: coarse_ndof x nvec */
+  int32_t nvec;
+  int64_t coarse_ndof;       /* hybrid: rows of near_nullspace_host */
+  const double* v0_host;     /* amg/hybrid power-method start vector */
 } tmg_mg_desc;
 int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
                               const int64_t* fixed_dofs_host, int64_t n_fixed,

@@ -37,7 +37,9 @@ class LevelInfo(C.Structure):
 
 class MgDesc(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("coarse_max_dofs", C.c_int64), ("max_levels", C.c_int32),
-                ("smoother", SmootherDesc), ("n_pre", C.c_int32), ("n_post", C.c_int32)]
+                ("smoother", SmootherDesc), ("n_pre", C.c_int32), ("n_post", C.c_int32),
+                ("n_geo", C.c_int32), ("beta", C.c_double), ("near_nullspace_host", C.c_void_p),
+                ("nvec", C.c_int32), ("coarse_ndof", C.c_int64), ("v0_host", C.c_void_p)]
 
 
 _P = C.c_void_p

@@ -281,8 +281,9 @@ int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_
   DevBuf<double> B, v0;
   B.alloc(nd * nvec, s);
   v0.alloc(nd, s);
-  TMG_CUDA(cudaMemcpyAsync(B.get(), B_host, nd * nvec * sizeof(double), cudaMemcpyHostToDevice, s));
-  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, nd * sizeof(double), cudaMemcpyHostToDevice, s));
+  // host or device pointers (unified addressing picks the direction)
+  TMG_CUDA(cudaMemcpyAsync(B.get(), B_host, nd * nvec * sizeof(double), cudaMemcpyDefault, s));
+  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, nd * sizeof(double), cudaMemcpyDefault, s));
   auto H = std::make_unique<tmg_hierarchy>();
   H->K = K;
   if (K->op.dim == 2)
@@ -307,8 +308,8 @@ int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* Bc_host, int6
   DevBuf<double> B, v0;
   B.alloc(coarse_ndof * nvec, s);
   v0.alloc(coarse_ndof, s);
-  TMG_CUDA(cudaMemcpyAsync(B.get(), Bc_host, coarse_ndof * nvec * sizeof(double), cudaMemcpyHostToDevice, s));
-  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, coarse_ndof * sizeof(double), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaMemcpyAsync(B.get(), Bc_host, coarse_ndof * nvec * sizeof(double), cudaMemcpyDefault, s));
+  TMG_CUDA(cudaMemcpyAsync(v0.get(), v0_host, coarse_ndof * sizeof(double), cudaMemcpyDefault, s));
   auto H = std::make_unique<tmg_hierarchy>();
   H->K = K;
   if (K->op.dim == 2)
@@ -559,7 +560,7 @@ int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
   ABI_BEGIN
   check_mesh(mesh);
   TMG_REQUIRE(mg && cfg, "mg/solve descriptor is NULL");
-  TMG_REQUIRE(mg->strategy == 0, "only strategy 0 (gmg) is available through this entry point");
+  TMG_REQUIRE(mg->strategy >= 0 && mg->strategy <= 2, "unknown preconditioner strategy");
   require_device();
   cudaStream_t s;
   TMG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -581,7 +582,14 @@ int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
   if (rc) return rc;
   std::unique_ptr<tmg_operator> Kg(K);
   tmg_hierarchy* H = nullptr;
-  rc = tmg_gmg_build(K, mg->coarse_max_dofs, mg->max_levels, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+  if (mg->strategy == 0)
+    rc = tmg_gmg_build(K, mg->coarse_max_dofs, mg->max_levels, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+  else if (mg->strategy == 1)
+    rc = tmg_sa_amg_build(K, mg->near_nullspace_host, mg->nvec, mg->coarse_max_dofs, mg->beta, mg->v0_host,
+                          &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+  else
+    rc = tmg_hybrid_build(K, mg->n_geo, mg->near_nullspace_host, mg->coarse_ndof, mg->nvec, mg->coarse_max_dofs,
+                          mg->beta, mg->v0_host, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
   if (rc) return rc;
   std::unique_ptr<tmg_hierarchy> Hg(H);
   rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);

@@ -233,21 +233,31 @@ def _start_vector(n, seed):
     return np.ascontiguousarray(np.random.default_rng(seed).standard_normal(n))
 
 
+def _host_or_device(a):
+    """(array, pointer): CUDA tensors are passed through, everything else becomes a
+    C-contiguous fp64 numpy array (the C ABI copies either kind)."""
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        a = a.contiguous()
+        return a, a.data_ptr()
+    a = np.ascontiguousarray(np.asarray(a, dtype=float))
+    return a, a.ctypes.data
+
+
 def build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0,
-                 beta=DEFAULT_STRENGTH_BETA, stream=None):
+                 beta=DEFAULT_STRENGTH_BETA, stream=None, v0=None):
     """Smoothed-aggregation hierarchy built on the device (multigrid.py:555).
-    EXTENSION: beta (the reference fixes 0.003)."""
+    EXTENSION: beta (the reference fixes 0.003); v0 overrides the power-method start
+    vector default_rng(seed).standard_normal(n) (e.g. a device-resident copy)."""
     smoother = smoother or SmootherConfig()
-    B = np.asarray(near_nullspace, dtype=float)
-    if B.ndim != 2 or B.shape[0] != K.shape[0]:
-        raise ValueError("near_nullspace must be (ndofs, nvec)")
     if smoother.kind not in SMOOTHER_KINDS:
         raise ValueError("unknown smoother kind %r" % smoother.kind)
-    B = np.ascontiguousarray(B)
-    v0 = _start_vector(K.shape[0], seed)
+    B, pB = _host_or_device(near_nullspace)
+    if B.ndim != 2 or B.shape[0] != K.shape[0]:
+        raise ValueError("near_nullspace must be (ndofs, nvec)")
+    v0, pv = _host_or_device(_start_vector(K.shape[0], seed) if v0 is None else v0)
     h = C.c_void_p()
-    _lib.check(_lib.load().tmg_sa_amg_build(K.handle, B.ctypes.data, B.shape[1], int(coarse_max_dofs),
-                                            float(beta), v0.ctypes.data, C.byref(smoother.desc()),
+    _lib.check(_lib.load().tmg_sa_amg_build(K.handle, pB, B.shape[1], int(coarse_max_dofs),
+                                            float(beta), pv, C.byref(smoother.desc()),
                                             int(n_pre), int(n_post), stream_ptr(stream), C.byref(h)))
     H = MgHierarchy(h, K, smoother, n_pre, n_post)
     H.flags = H.device_flags()

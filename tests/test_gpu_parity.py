@@ -37,7 +37,12 @@ def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
     implementation; tests use max(tolerance, 10 x floor) and say so."""
     u1, r1 = O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit)
     u2, r2 = O.pcg(_Transposed(Kref), f, None, M, rtol=rtol, max_iterations=maxit)
-    return rel(u2, u1), abs(f @ u2 - f @ u1) / abs(f @ u1)
+    return rel(u2, u1), abs(f @ u2 - f @ u1) / abs(f @ u1), abs(r1.iterations - r2.iterations)
+
+
+def iteration_tolerance(floor_it):
+    """+-1 (north star), widened to the oracle's own order-of-summation spread."""
+    return max(1, 2 * floor_it)
 
 
 def host(t):
@@ -147,8 +152,8 @@ def test_pcg_matches_oracle(dims, levels, kind, void):
     u, rec = T.cg_solve(K, bc.load_vector, None, h, cfg)
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=2000)
     assert rec.converged and reco.converged
-    assert abs(rec.iterations - reco.iterations) <= 1
-    fu, fc = reproducibility_floor(Kref, bc.load_vector, ho.apply)
+    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply)
+    assert abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
     assert rel(host(u), uo) <= max(1e-8, 10 * fu)
     c, co = float(bc.load_vector @ host(u)), float(bc.load_vector @ uo)
     assert abs(c - co) <= max(1e-10, 10 * fc) * abs(co), (abs(c - co) / abs(co), fc)
@@ -167,8 +172,8 @@ def test_jacobi_safeguard_matches_oracle():
     assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-10
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
-    assert rec.converged and abs(rec.iterations - reco.iterations) <= 1
-    fu, fc = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
+    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
+    assert rec.converged and abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
     assert rel(host(u), uo) <= max(1e-8, 10 * fu)
 
 
