@@ -23,6 +23,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include "tmg_bsr.cuh"
 
@@ -506,22 +507,89 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __res
   for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
   __syncwarp();
   int mine = 0;
-  for (int p = xp[row]; p < xp[row + 1]; ++p) {
+  bool full = false;
+  for (int p = xp[row]; p < xp[row + 1] && !full; ++p) {
     const int k = xc[p];
     for (int q = yp[k] + lane; q < yp[k + 1]; q += 32) {
       const int j = yc[q];
       unsigned h = ((unsigned)j * 2654435761u) & (SG_SLOTS - 1);
       for (int probe = 0;; ++probe) {
-        if (probe == SG_SLOTS) { atomicOr(overflow, 1); break; }
+        if (probe == SG_SLOTS) { full = true; break; }
         const int prev = atomicCAS(&set[w][h], -1, j);
         if (prev == -1) { ++mine; break; }
         if (prev == j) break;
         h = (h + 1) & (SG_SLOTS - 1);
       }
+      if (full) break;
     }
+    full = __any_sync(0xffffffffu, full);
   }
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
-  if (lane == 0) cnt[row] = mine;
+  if (lane == 0) {
+    cnt[row] = full ? 0 : mine;
+    if (full) {
+      overflow[row] = 1;  // heavy row: handled by the global-memory path
+    }
+  }
+}
+
+// ---- heavy rows (more distinct columns than the shared-memory set holds; e.g. the
+// aggregate that absorbs all isolated nodes, multigrid.py:457-467) ----
+__global__ void k_heavy_bound(const int* __restrict__ xp, const int* __restrict__ xc, const int* __restrict__ yp,
+                              int row, unsigned long long* __restrict__ bound) {
+  unsigned long long b = 0;
+  for (int p = xp[row] + threadIdx.x; p < xp[row + 1]; p += blockDim.x) b += yp[xc[p] + 1] - yp[xc[p]];
+  atomicAdd(bound, b);
+}
+__global__ void k_heavy_gather(const int* __restrict__ xp, const int* __restrict__ xc, const int* __restrict__ yp,
+                               const int* __restrict__ yc, int row, int* __restrict__ out,
+                               unsigned long long* __restrict__ pos) {
+  for (int p = xp[row] + blockIdx.x; p < xp[row + 1]; p += gridDim.x) {
+    const int k = xc[p];
+    const int len = yp[k + 1] - yp[k];
+    __shared__ unsigned long long base;
+    if (threadIdx.x == 0) base = atomicAdd(pos, (unsigned long long)len);
+    __syncthreads();
+    for (int q = threadIdx.x; q < len; q += blockDim.x) out[base + q] = yc[yp[k] + q];
+    __syncthreads();
+  }
+}
+// values of a heavy row whose sorted column list is already in cc[cp[row] ...]
+template <int R1, int K1, int C2>
+__global__ void k_heavy_fill(const int* __restrict__ xp, const int* __restrict__ xc, const double* __restrict__ xv,
+                             const int* __restrict__ yp, const int* __restrict__ yc, const double* __restrict__ yv,
+                             int row, const int* __restrict__ cp, const int* __restrict__ cc, double* __restrict__ cv) {
+  const int base = cp[row], nout = cp[row + 1] - base;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= nout) return;
+  const int j = cc[base + o];
+  double acc[R1 * C2];
+#pragma unroll
+  for (int t = 0; t < R1 * C2; ++t) acc[t] = 0.0;
+  for (int p = xp[row]; p < xp[row + 1]; ++p) {
+    const int k = xc[p];
+    int lo = yp[k], hi = yp[k + 1] - 1, hit = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1, v = yc[mid];
+      if (v == j) { hit = mid; break; }
+      if (v < j) lo = mid + 1; else hi = mid - 1;
+    }
+    if (hit < 0) continue;
+    const double* X = xv + (long long)p * R1 * K1;
+    const double* Y = yv + (long long)hit * K1 * C2;
+#pragma unroll
+    for (int a = 0; a < R1; ++a)
+#pragma unroll
+      for (int b = 0; b < C2; ++b) {
+        double s = acc[a * C2 + b];
+#pragma unroll
+        for (int c = 0; c < K1; ++c) s += X[a * K1 + c] * Y[c * C2 + b];
+        acc[a * C2 + b] = s;
+      }
+  }
+  double* out = cv + (long long)(base + o) * R1 * C2;
+#pragma unroll
+  for (int t = 0; t < R1 * C2; ++t) out[t] = acc[t];
 }
 // Numeric SpGEMM: collect the row's distinct columns (sorted), then each output
 // block C_ij = sum_k X_ik Y_kj with k ascending (deterministic).
@@ -531,11 +599,12 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_fill(const int* __rest
                                                                 const int* __restrict__ yp, const int* __restrict__ yc,
                                                                 const double* __restrict__ yv, int nrows,
                                                                 const int* __restrict__ cp, int* __restrict__ cc,
-                                                                double* __restrict__ cv) {
+                                                                double* __restrict__ cv,
+                                                                const int* __restrict__ heavy) {
   __shared__ int set[SG_WARPS][SG_SLOTS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * SG_WARPS + w;
-  if (row >= nrows) return;
+  if (row >= nrows || heavy[row]) return;
   for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
   __syncwarp();
   for (int p = xp[row]; p < xp[row + 1]; ++p) {

@@ -76,24 +76,68 @@ inline void bsr_spgemm(const Bsr& X, const Bsr& Y, Bsr& Cm, cudaStream_t s) {
   Cm.ncols = Y.ncols;
   Cm.R = X.R;
   Cm.C = Y.C;
-  DevBuf<int> cnt, ovf;
+  DevBuf<int> cnt, heavy;
   cnt.alloc(n + 1, s);
   cnt.zero(s);
-  ovf.alloc(1, s);
-  ovf.zero(s);
+  heavy.alloc(n, s);
+  heavy.zero(s);
   const unsigned g = (unsigned)((n + SG_WARPS - 1) / SG_WARPS);
   k_spgemm_count<<<g, SG_WARPS * 32, 0, s>>>(X.rowptr.get(), X.col.get(), Y.rowptr.get(), Y.col.get(), n, cnt.get(),
-                                             ovf.get());
-  TMG_REQUIRE(read_int(ovf.get(), s) == 0, "Galerkin product row exceeds the SpGEMM hash capacity");
+                                             heavy.get());
+  note_launch();
+  // rows whose column set overflows the shared-memory hash: sort+unique in global memory
+  std::vector<int> hheavy(n);
+  TMG_CUDA(cudaMemcpyAsync(hheavy.data(), heavy.get(), n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> heavy_rows;
+  for (int r = 0; r < n; ++r)
+    if (hheavy[r]) heavy_rows.push_back(r);
+  std::vector<DevBuf<int>> heavy_cols(heavy_rows.size());
+  std::vector<int> heavy_n(heavy_rows.size());
+  for (size_t t = 0; t < heavy_rows.size(); ++t) {
+    const int r = heavy_rows[t];
+    DevBuf<unsigned long long> bnd, pos;
+    bnd.alloc(1, s); bnd.zero(s); pos.alloc(1, s); pos.zero(s);
+    k_heavy_bound<<<1, 256, 0, s>>>(X.rowptr.get(), X.col.get(), Y.rowptr.get(), r, bnd.get());
+    unsigned long long hb = 0;
+    TMG_CUDA(cudaMemcpyAsync(&hb, bnd.get(), sizeof(hb), cudaMemcpyDeviceToHost, s));
+    TMG_CUDA(cudaStreamSynchronize(s));
+    DevBuf<int> cand, sorted, nsel;
+    cand.alloc(hb, s); sorted.alloc(hb, s); nsel.alloc(1, s);
+    heavy_cols[t].alloc(hb, s);
+    k_heavy_gather<<<1024, 256, 0, s>>>(X.rowptr.get(), X.col.get(), Y.rowptr.get(), Y.col.get(), r, cand.get(),
+                                        pos.get());
+    size_t tb = 0;
+    TMG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, cand.get(), sorted.get(), (int)hb, 0, 32, s));
+    size_t tb2 = 0;
+    TMG_CUDA(cub::DeviceSelect::Unique(nullptr, tb2, sorted.get(), heavy_cols[t].get(), nsel.get(), (int)hb, s));
+    DevBuf<char> tmp;
+    tmp.alloc(std::max(tb, tb2), s);
+    TMG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), tb, cand.get(), sorted.get(), (int)hb, 0, 32, s));
+    TMG_CUDA(cub::DeviceSelect::Unique(tmp.get(), tb2, sorted.get(), heavy_cols[t].get(), nsel.get(), (int)hb, s));
+    TMG_CUDA(cudaMemcpyAsync(cnt.get() + r, nsel.get(), sizeof(int), cudaMemcpyDeviceToDevice, s));
+    heavy_n[t] = read_int(nsel.get(), s);
+    note_launch(2);
+  }
   rowptr_from_counts(cnt, Cm.rowptr, n, s);
   Cm.nnzb = read_int(Cm.rowptr.get() + n, s);
   Cm.col.alloc(std::max<long long>(Cm.nnzb, 1), s);
   Cm.val.alloc(std::max<long long>(Cm.nnzb, 1) * Cm.R * Cm.C, s);
+  for (size_t t = 0; t < heavy_rows.size(); ++t) {
+    const int off = read_int(Cm.rowptr.get() + heavy_rows[t], s);
+    TMG_CUDA(cudaMemcpyAsync(Cm.col.get() + off, heavy_cols[t].get(), heavy_n[t] * sizeof(int),
+                             cudaMemcpyDeviceToDevice, s));
+  }
 #define TMG_SPGEMM_CASE(a, b, c)                                                                               \
   if (X.R == a && X.C == b && Y.C == c) {                                                                       \
     k_spgemm_fill<a, b, c><<<g, SG_WARPS * 32, 0, s>>>(X.rowptr.get(), X.col.get(), X.val.get(), Y.rowptr.get(), \
                                                        Y.col.get(), Y.val.get(), n, Cm.rowptr.get(), Cm.col.get(), \
-                                                       Cm.val.get());                                          \
+                                                       Cm.val.get(), heavy.get());                             \
+    for (size_t t = 0; t < heavy_rows.size(); ++t)                                                              \
+      k_heavy_fill<a, b, c><<<grid_for(heavy_n[t]), TPB, 0, s>>>(X.rowptr.get(), X.col.get(), X.val.get(),      \
+                                                                 Y.rowptr.get(), Y.col.get(), Y.val.get(),      \
+                                                                 heavy_rows[t], Cm.rowptr.get(), Cm.col.get(),  \
+                                                                 Cm.val.get());                                 \
   } else
   TMG_SPGEMM_CASE(2, 2, 3)
   TMG_SPGEMM_CASE(3, 2, 3)

@@ -21,6 +21,11 @@ from .mesh import BoundaryConditions, build_mesh
 
 E0, EMIN, NU, PENAL = 1.0, 1e-9, 0.3, 3.0
 VOID = 1e-3
+# "symmetric strength threshold 0.08" is theta in ||A_IJ|| > theta sqrt(||A_II|| ||A_JJ||);
+# the reference's rule (multigrid.py:355) is the squared form ||A_IJ||^2 > beta ..., so
+# beta = theta^2.  (beta = 0.08 literally would isolate 98% of config 1's nodes.)
+THETA = 0.08
+BETA = THETA * THETA
 
 
 @dataclass
@@ -116,7 +121,7 @@ def config_1(seed=1655):
                     # reports the converged flag -- the paper's GMG failure mode.
                     solvers=[dict(strategy="gmg", levels=5, smoother="weighted_jacobi", weight=0.6,
                                   n_pre=2, n_post=2, safeguard=1.8, max_iterations=2000),
-                             dict(strategy="amg", coarse_max_dofs=499, beta=0.08,
+                             dict(strategy="amg", coarse_max_dofs=499, beta=BETA,
                                   smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2)])
 
 
@@ -147,7 +152,7 @@ def config_2(seed=2001):
     loads.append(f)
     bc = BoundaryConditions(np.array(fixed), loads[0])
     return Workload("cantilever2d_1920x640_amg_4loads", mesh, bc, to_elements(rho), loads=loads[1:],
-                    solvers=[dict(strategy="amg", coarse_max_dofs=499, beta=0.08,
+                    solvers=[dict(strategy="amg", coarse_max_dofs=499, beta=BETA,
                                   smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2)])
 
 
@@ -179,7 +184,7 @@ def config_4(seed=4004):
     g = gaussian_field((nx, ny, nz), 10.0, seed)
     rho = cone_filter(threshold(g, 0.12), 1.5)
     return Workload("cantilever3d_192x96x96_hybrid", mesh, bc, to_elements(rho),
-                    solvers=[dict(strategy="hybrid", n_geo=3, coarse_max_dofs=999, beta=0.08,
+                    solvers=[dict(strategy="hybrid", n_geo=3, coarse_max_dofs=999, beta=BETA,
                                   smoother="chebyshev", degree=2, lanczos_steps=10, n_pre=1, n_post=1)])
 
 
