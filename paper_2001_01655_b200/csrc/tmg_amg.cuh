@@ -465,6 +465,33 @@ __global__ void k_smooth_p(BsrView<BS, BS> A, const int* __restrict__ agg, const
   }
 }
 
+// P from AT = A*T (same sparsity: A_ii != 0 puts agg(i) in every row of AT):
+// P_iJ = [J == agg(i)] T_i - (omega D_i^-1) (AT)_iJ, in place on AT's values.
+template <int BS, int NV>
+__global__ void k_p_from_at(int nrows, const int* __restrict__ rowptr, const int* __restrict__ col,
+                            double* __restrict__ val, const int* __restrict__ agg, const double* __restrict__ Tval,
+                            const double* __restrict__ dinv, const double* __restrict__ rho) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const double omega = 4.0 / (3.0 * fmax(*rho, 1e-30));
+  double ds[BS];
+#pragma unroll
+  for (int r = 0; r < BS; ++r) ds[r] = __dmul_rn(omega, dinv[(long long)row * BS + r]);
+  const int own = agg[row];
+  const double* tr = Tval + (long long)row * BS * NV;
+  for (int p = rowptr[row]; p < rowptr[row + 1]; ++p) {
+    double* v = val + (long long)p * BS * NV;
+    const bool mine = col[p] == own;
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        const double x = __dmul_rn(ds[r], v[r * NV + c]);
+        v[r * NV + c] = mine ? __dsub_rn(tr[r * NV + c], x) : -x;
+      }
+  }
+}
+
 // ----------------------------------------------------------------------------
 // BSR transpose and SpGEMM
 // ----------------------------------------------------------------------------

@@ -341,29 +341,14 @@ inline void spectral_radius(Hierarchy& H, const Bsr& A, int bs, const double* di
   note_launch(2);
 }
 
+// P = T - omega D^-1 (A T): AT by the BSR SpGEMM (heavy rows included), then the
+// scaling/own-block update in place (multigrid.py:518-525).
 template <int BS, int NV>
 void smooth_p_typed(const Bsr& A, const Level& l, const double* dinv, Bsr& P, cudaStream_t s) {
-  const int n = A.nrows;
-  P.nrows = n;
-  P.ncols = l.n_agg;
-  P.R = BS;
-  P.C = NV;
-  DevBuf<int> cnt, ovf;
-  cnt.alloc(n + 1, s);
-  cnt.zero(s);
-  ovf.alloc(1, s);
-  ovf.zero(s);
-  k_smooth_p<BS, NV, false><<<grid_for(n), TPB, 0, s>>>(view<BS, BS>(A), l.agg.get(), l.Tm.val.get(), dinv,
-                                                        l.rho.get(), cnt.get(), nullptr, nullptr, nullptr, ovf.get());
-  TMG_REQUIRE(read_int(ovf.get(), s) == 0, "prolongation row touches too many aggregates");
-  rowptr_from_counts(cnt, P.rowptr, n, s);
-  P.nnzb = read_int(P.rowptr.get() + n, s);
-  P.col.alloc(P.nnzb, s);
-  P.val.alloc(P.nnzb * BS * NV, s);
-  k_smooth_p<BS, NV, true><<<grid_for(n), TPB, 0, s>>>(view<BS, BS>(A), l.agg.get(), l.Tm.val.get(), dinv,
-                                                       l.rho.get(), nullptr, P.rowptr.get(), P.col.get(),
-                                                       P.val.get(), ovf.get());
-  note_launch(2);
+  bsr_spgemm(A, l.Tm, P, s);
+  k_p_from_at<BS, NV><<<grid_for(P.nrows), TPB, 0, s>>>(P.nrows, P.rowptr.get(), P.col.get(), P.val.get(),
+                                                        l.agg.get(), l.Tm.val.get(), dinv, l.rho.get());
+  note_launch();
   TMG_CUDA(cudaGetLastError());
 }
 inline void smooth_p(const Bsr& A, const Level& l, const double* dinv, int bs, int nv, Bsr& P, cudaStream_t s) {
