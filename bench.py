@@ -129,10 +129,10 @@ def oracle_sample(w, leg, iters):
         h = O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
     elif leg["strategy"] == "amg":
         h = O.build_sa_amg(K, O.rigid_body_modes(g, w.bc.fixed_dofs), leg["coarse_max_dofs"], sm, leg["n_pre"],
-                           leg["n_post"], beta=leg["beta"])
+                           leg["n_post"], beta=leg["beta"], isolated=leg.get("isolated", "merge"))
     else:
         h = O.build_hybrid(g, K, O.rigid_body_modes(g, w.bc.fixed_dofs), leg["n_geo"], leg["coarse_max_dofs"], sm,
-                           leg["n_pre"], leg["n_post"], beta=leg["beta"])
+                           leg["n_pre"], leg["n_post"], beta=leg["beta"], isolated=leg.get("isolated", "merge"))
     u, rec = O.pcg(K, w.bc.load_vector, None, h.apply, rtol=w.rtol, max_iterations=iters)
     O.compliance_sensitivity(g, w.bc.load_vector, u, w.rho, problems.PENAL, problems.E0, problems.EMIN)
     dt = time.perf_counter() - t0
@@ -182,6 +182,7 @@ class LegRunner:
         self.name = problems.leg_name(leg)
         self.sm = problems.smoother_settings(leg)
         self.maxit = leg.get("max_iterations", 10000)
+        self.isolated = leg.get("isolated", "merge")
         if leg["strategy"] == "amg":
             B = T.rigid_body_modes(w.mesh, w.bc.fixed_dofs)
             self.B = torch.as_tensor(B, device="cuda")
@@ -195,15 +196,16 @@ class LegRunner:
             return T.build_gmg(w.mesh, K, 1, self.sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
         if leg["strategy"] == "amg":
             return T.build_sa_amg(K, self.B, leg["coarse_max_dofs"], self.sm, leg["n_pre"], leg["n_post"],
-                                  beta=leg["beta"], v0=self.v0)
+                                  beta=leg["beta"], v0=self.v0, isolated=self.isolated)
         return T.build_hybrid(w.mesh, K, self.B, leg["n_geo"], leg["coarse_max_dofs"], self.sm, leg["n_pre"],
-                              leg["n_post"], beta=leg["beta"])
+                              leg["n_post"], beta=leg["beta"], isolated=self.isolated)
 
     def mg_desc(self):
         """tmg_mg_desc for the host-buffer entry point (+ keep-alive host arrays)."""
         from paper_2001_01655_b200 import _lib
         from paper_2001_01655_b200.mesh import StructuredMesh, rigid_body_modes
         from paper_2001_01655_b200.multigrid import hybrid_plan
+        from paper_2001_01655_b200.multigrid import isolated_mode as T_isolated_mode
         leg, w = self.leg, self.w
         mg = _lib.MgDesc()
         mg.strategy = {"gmg": 0, "amg": 1, "hybrid": 2}[leg["strategy"]]
@@ -228,6 +230,7 @@ class LegRunner:
             mg.nvec = keep[0].shape[1]
             mg.coarse_ndof = keep[0].shape[0]
             mg.v0_host = keep[1].ctypes.data
+            mg.isolated_mode = T_isolated_mode(self.isolated)
         return mg, keep
 
 

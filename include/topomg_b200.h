@@ -123,14 +123,17 @@ int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels,
 int tmg_sa_amg_build(tmg_operator* K, const double* near_nullspace_host, int32_t nvec,
                      int64_t coarse_max_dofs, double beta, const double* v0_host,
                      const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
-                     void* stream, tmg_hierarchy** out);
+                     int32_t isolated_mode, void* stream, tmg_hierarchy** out);
+/* isolated_mode 0: reference behaviour (multigrid.py:418-423, 457-467: strength-
+ * isolated nodes become singletons that the fallback folds into one aggregate);
+ * 1 (extension): they stay unaggregated (zero rows of T), PyAMG-style. */
 /* multigrid.py:573 build_hybrid(mesh, K, near_nullspace, n_geo, ...) for n_geo >= 1:
  * coarse_near_nullspace_host = rigid_body_modes(coarse_mesh) of the mesh reached
  * after the geometric levels (coarse_ndof rows), v0_host its start vector. */
 int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* coarse_near_nullspace_host,
                      int64_t coarse_ndof, int32_t nvec, int64_t coarse_max_dofs, double beta,
                      const double* v0_host, const tmg_smoother_desc* smoother, int32_t n_pre,
-                     int32_t n_post, void* stream, tmg_hierarchy** out);
+                     int32_t n_post, int32_t isolated_mode, void* stream, tmg_hierarchy** out);
 /* MgHierarchy.flags as a comma-separated list. */
 int tmg_hierarchy_flags(const tmg_hierarchy* h, char* buf, int32_t cap);
 /* Export level data for parity checks (two-call: NULL buffers return dims only).
@@ -187,6 +190,7 @@ typedef struct {
   int32_t nvec;
   int64_t coarse_ndof;       /* hybrid: rows of near_nullspace_host */
   const double* v0_host;     /* amg/hybrid power-method start vector */
+  int32_t isolated_mode;     /* amg/hybrid: 0 reference merge, 1 drop (see tmg_sa_amg_build) */
 } tmg_mg_desc;
 int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
                               const int64_t* fixed_dofs_host, int64_t n_fixed,

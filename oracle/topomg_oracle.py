@@ -577,8 +577,12 @@ def strength_graph(K, beta=BETA_DEFAULT, block_size=1):
     return sp.csr_matrix((np.ones(keep.sum()), (C.row[keep], C.col[keep])), shape=(nb, nb))
 
 
-def aggregate(adj):
-    """Greedy root pass, neighbour absorption, isolated/forced fallbacks (multigrid.py:380)."""
+def aggregate(adj, isolated="merge"):
+    """Greedy root pass, neighbour absorption, isolated/forced fallbacks (multigrid.py:380).
+
+    EXTENSION isolated="drop": nodes without strong connections stay unaggregated
+    (id -1, zero rows of T -- PyAMG standard_aggregation semantics) instead of
+    becoming singletons that _merge_small_aggregates folds into ONE aggregate."""
     n = adj.shape[0]
     ptr, ind = adj.indptr, adj.indices
     agg = -np.ones(n, np.int64)
@@ -603,15 +607,24 @@ def aggregate(adj):
     if count == 0 or count + lone.size >= n:
         return np.arange(n) // 2, ["forced_pairwise_aggregation"]
     if lone.size:
-        agg[lone] = count + np.arange(lone.size)
+        if isolated == "merge":
+            agg[lone] = count + np.arange(lone.size)
         flags.append("isolated_nodes")
     return agg, flags
 
 
+def _renumber(agg):
+    """np.unique(agg, return_inverse=True) over the aggregated nodes (-1 kept)."""
+    out = agg.copy()
+    m = agg >= 0
+    out[m] = np.unique(agg[m], return_inverse=True)[1]
+    return out
+
+
 def merge_small(agg, adj, min_size):
     """Fold undersized aggregates into a strong neighbour, else an index neighbour
-    (multigrid.py:427)."""
-    size = np.bincount(agg)
+    (multigrid.py:427).  Unaggregated (-1) nodes are left alone (EXTENSION)."""
+    size = np.bincount(agg[agg >= 0])
     small = np.flatnonzero(size < min_size)
     if small.size == 0:
         return agg
@@ -622,7 +635,7 @@ def merge_small(agg, adj, min_size):
         tgt = -1
         for i in members:
             for j in ind[ptr[i]:ptr[i + 1]]:
-                if agg[j] != a and size[agg[j]] >= min_size:
+                if agg[j] != a and agg[j] >= 0 and size[agg[j]] >= min_size:
                     tgt = agg[j]
                     break
             if tgt >= 0:
@@ -631,9 +644,9 @@ def merge_small(agg, adj, min_size):
             agg[members] = tgt
             size[tgt] += members.size
             size[a] = 0
-    agg = np.unique(agg, return_inverse=True)[1]
+    agg = _renumber(agg)
     while True:
-        size = np.bincount(agg)
+        size = np.bincount(agg[agg >= 0])
         if size.size < 2:
             break
         small = np.flatnonzero(size < min_size)
@@ -641,7 +654,7 @@ def merge_small(agg, adj, min_size):
             break
         a = small[0]
         agg[agg == a] = a - 1 if a > 0 else a + 1
-        agg = np.unique(agg, return_inverse=True)[1]
+        agg = _renumber(agg)
     return agg
 
 
@@ -692,14 +705,14 @@ def smooth_prolongation(A, T, seed=0):
 
 
 def sa_levels(A, B, coarse_max_dofs, smoother, block_size, flags, max_levels=30, seed=0,
-              beta=BETA_DEFAULT):
-    """multigrid.py:528; EXTENSION: beta parameter (reference fixes 0.003)."""
+              beta=BETA_DEFAULT, isolated="merge"):
+    """multigrid.py:528; EXTENSION: beta parameter (reference fixes 0.003), isolated mode."""
     levels = []
     nv = B.shape[1]
     while A.shape[0] > coarse_max_dofs and len(levels) < max_levels:
         min_nodes = max(2, -(-nv // block_size))
         S = strength_graph(A, beta, block_size)
-        agg, f = aggregate(S)
+        agg, f = aggregate(S, isolated)
         flags.extend(f)
         agg = merge_small(agg, S, min_nodes)
         if (int(agg.max()) + 1) * nv >= A.shape[0]:
@@ -717,7 +730,7 @@ def sa_levels(A, B, coarse_max_dofs, smoother, block_size, flags, max_levels=30,
 
 
 def build_sa_amg(K, B, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0,
-                 beta=BETA_DEFAULT):
+                 beta=BETA_DEFAULT, isolated="merge"):
     smoother = smoother or Smoother()
     B = np.asarray(B, float)
     if B.ndim != 2 or B.shape[0] != K.shape[0]:
@@ -725,16 +738,16 @@ def build_sa_amg(K, B, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0
     bs = {3: 2, 6: 3}.get(B.shape[1], 1)
     flags = []
     levels = sa_levels(sp.csr_matrix(K), B, coarse_max_dofs, smoother, bs, flags, seed=seed,
-                       beta=beta)
+                       beta=beta, isolated=isolated)
     return finalize(levels, n_pre, n_post, flags, smoother)
 
 
 def build_hybrid(grid, K, B, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_post=1,
-                 seed=0, beta=BETA_DEFAULT):
+                 seed=0, beta=BETA_DEFAULT, isolated="merge"):
     """Geometric on the finest n_geo levels, SA below (multigrid.py:573)."""
     smoother = smoother or Smoother()
     if n_geo <= 0:
-        return build_sa_amg(K, B, coarse_max_dofs, smoother, n_pre, n_post, seed, beta)
+        return build_sa_amg(K, B, coarse_max_dofs, smoother, n_pre, n_post, seed, beta, isolated)
     flags, levels = [], []
     A = sp.csr_matrix(K)
     dims, h = grid.dims, grid.h
@@ -751,7 +764,7 @@ def build_hybrid(grid, K, B, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_p
         h = tuple(2 * x for x in h)
     cgrid = Grid(dims, h)
     levels += sa_levels(A, rigid_body_modes(cgrid), coarse_max_dofs, smoother, cgrid.dpn,
-                        flags, seed=seed, beta=beta)
+                        flags, seed=seed, beta=beta, isolated=isolated)
     return finalize(levels, n_pre, n_post, flags, smoother)
 
 

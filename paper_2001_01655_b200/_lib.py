@@ -39,7 +39,8 @@ class MgDesc(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("coarse_max_dofs", C.c_int64), ("max_levels", C.c_int32),
                 ("smoother", SmootherDesc), ("n_pre", C.c_int32), ("n_post", C.c_int32),
                 ("n_geo", C.c_int32), ("beta", C.c_double), ("near_nullspace_host", C.c_void_p),
-                ("nvec", C.c_int32), ("coarse_ndof", C.c_int64), ("v0_host", C.c_void_p)]
+                ("nvec", C.c_int32), ("coarse_ndof", C.c_int64), ("v0_host", C.c_void_p),
+                ("isolated_mode", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -60,9 +61,10 @@ _SIGS = {
     "tmg_gmg_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.POINTER(SmootherDesc), C.c_int32,
                                 C.c_int32, _P, C.POINTER(_P)]),
     "tmg_sa_amg_build": (C.c_int, [_P, _P, C.c_int32, C.c_int64, C.c_double, _P, C.POINTER(SmootherDesc),
-                                   C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+                                   C.c_int32, C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
     "tmg_hybrid_build": (C.c_int, [_P, C.c_int32, _P, C.c_int64, C.c_int32, C.c_int64, C.c_double, _P,
-                                   C.POINTER(SmootherDesc), C.c_int32, C.c_int32, _P, C.POINTER(_P)]),
+                                   C.POINTER(SmootherDesc), C.c_int32, C.c_int32, C.c_int32, _P,
+                                   C.POINTER(_P)]),
     "tmg_hierarchy_flags": (C.c_int, [_P, C.c_char_p, C.c_int32]),
     "tmg_hierarchy_export": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P]),
     "tmg_hierarchy_destroy": (C.c_int, [_P]),
@@ -71,7 +73,7 @@ _SIGS = {
     "tmg_hierarchy_vcycle": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tmg_hierarchy_level_apply": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tmg_hierarchy_level_lmax": (C.c_int, [_P, C.c_int32, _D, _P]),
-"tmg_hierarchy_time_smoother": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _P]),
+    "tmg_hierarchy_time_smoother": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _P]),
     "tmg_pcg_solve": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolveDesc), _P,
                                 C.POINTER(SolveRec), _P]),
     "tmg_strain_energy": (C.c_int, [_P, _P, _P, _P]),

@@ -270,9 +270,10 @@ int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels, 
 
 int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_t coarse_max_dofs, double beta,
                      const double* v0_host, const tmg_smoother_desc* smoother, int32_t n_pre, int32_t n_post,
-                     void* stream, tmg_hierarchy** out) {
+                     int32_t isolated_mode, void* stream, tmg_hierarchy** out) {
   ABI_BEGIN
   TMG_REQUIRE(K && B_host && v0_host, "operator/near_nullspace/start vector is NULL");
+  TMG_REQUIRE(isolated_mode == 0 || isolated_mode == 1, "isolated_mode must be 0 (merge) or 1 (drop)");
   TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
   TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
   const SmootherCfg c = to_cfg(smoother);
@@ -287,9 +288,11 @@ int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_
   auto H = std::make_unique<tmg_hierarchy>();
   H->K = K;
   if (K->op.dim == 2)
-    H->h = build_sa_amg<2>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post, s);
+    H->h = build_sa_amg<2>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
+                           isolated_mode == 1, s);
   else
-    H->h = build_sa_amg<3>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post, s);
+    H->h = build_sa_amg<3>(K->op, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
+                           isolated_mode == 1, s);
   TMG_CUDA(cudaStreamSynchronize(s));
   *out = H.release();
   ABI_END
@@ -297,9 +300,10 @@ int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_
 
 int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* Bc_host, int64_t coarse_ndof, int32_t nvec,
                      int64_t coarse_max_dofs, double beta, const double* v0_host, const tmg_smoother_desc* smoother,
-                     int32_t n_pre, int32_t n_post, void* stream, tmg_hierarchy** out) {
+                     int32_t n_pre, int32_t n_post, int32_t isolated_mode, void* stream, tmg_hierarchy** out) {
   ABI_BEGIN
   TMG_REQUIRE(K && Bc_host && v0_host, "operator/near_nullspace/start vector is NULL");
+  TMG_REQUIRE(isolated_mode == 0 || isolated_mode == 1, "isolated_mode must be 0 (merge) or 1 (drop)");
   TMG_REQUIRE(n_geo >= 1, "n_geo must be >= 1 (n_geo = 0 is build_sa_amg)");
   TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
   TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
@@ -314,10 +318,10 @@ int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* Bc_host, int6
   H->K = K;
   if (K->op.dim == 2)
     H->h = build_hybrid<2>(K->op, n_geo, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
-                           coarse_ndof, s);
+                           coarse_ndof, isolated_mode == 1, s);
   else
     H->h = build_hybrid<3>(K->op, n_geo, B.get(), nvec, coarse_max_dofs, beta, v0.get(), c, n_pre, n_post,
-                           coarse_ndof, s);
+                           coarse_ndof, isolated_mode == 1, s);
   TMG_CUDA(cudaStreamSynchronize(s));
   *out = H.release();
   ABI_END
@@ -586,10 +590,10 @@ int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
     rc = tmg_gmg_build(K, mg->coarse_max_dofs, mg->max_levels, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
   else if (mg->strategy == 1)
     rc = tmg_sa_amg_build(K, mg->near_nullspace_host, mg->nvec, mg->coarse_max_dofs, mg->beta, mg->v0_host,
-                          &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+                          &mg->smoother, mg->n_pre, mg->n_post, mg->isolated_mode, s, &H);
   else
     rc = tmg_hybrid_build(K, mg->n_geo, mg->near_nullspace_host, mg->coarse_ndof, mg->nvec, mg->coarse_max_dofs,
-                          mg->beta, mg->v0_host, &mg->smoother, mg->n_pre, mg->n_post, s, &H);
+                          mg->beta, mg->v0_host, &mg->smoother, mg->n_pre, mg->n_post, mg->isolated_mode, s, &H);
   if (rc) return rc;
   std::unique_ptr<tmg_hierarchy> Hg(H);
   rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);

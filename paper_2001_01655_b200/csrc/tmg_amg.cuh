@@ -203,6 +203,21 @@ __global__ void k_assign_isolated(int n, const int* __restrict__ rank_iso, int b
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] == -1) agg[i] = base + rank_iso[i];
 }
+__global__ void k_flag_nonneg(const int* __restrict__ v, int n, int* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v[i] >= 0 ? 1 : 0;
+}
+// BSR T from the node-indexed blocks: one block per aggregated node, none for
+// unaggregated (-1) nodes
+__global__ void k_compact_T(int n, const int* __restrict__ agg, const int* __restrict__ rowptr,
+                            const double* __restrict__ Tnode, int bsnv, int* __restrict__ col,
+                            double* __restrict__ val) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || agg[i] < 0) return;
+  const int p = rowptr[i];
+  col[p] = agg[i];
+  for (int t = 0; t < bsnv; ++t) val[(long long)p * bsnv + t] = Tnode[(long long)i * bsnv + t];
+}
 __global__ void k_fill_value_where(int* __restrict__ agg, int n, int from, int to) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] == from) agg[i] = to;
@@ -213,7 +228,7 @@ __global__ void k_pairwise(int* __restrict__ agg, int n) {
 }
 __global__ void k_histogram(const int* __restrict__ agg, int n, int* __restrict__ size) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(size + agg[i], 1);
+  if (i < n && agg[i] >= 0) atomicAdd(size + agg[i], 1);
 }
 
 // Exact sequential _merge_small_aggregates (multigrid.py:427-468) for the general
@@ -233,7 +248,7 @@ __global__ void k_merge_small_seq(const int* __restrict__ sptr, const int* __res
       if (agg[i] != a) continue;
       for (int p = sptr[i]; p < sptr[i + 1]; ++p) {
         const int j = scol[p];
-        if (agg[j] != a && size[agg[j]] >= min_size) { tgt = agg[j]; break; }
+        if (agg[j] != a && agg[j] >= 0 && size[agg[j]] >= min_size) { tgt = agg[j]; break; }
       }
     }
     if (tgt >= 0) {
@@ -247,12 +262,14 @@ __global__ void k_merge_small_seq(const int* __restrict__ sptr, const int* __res
   // np.unique(return_inverse) renumbering + fallback folding into index neighbours
   while (true) {
     for (int a = 0; a < n_agg; ++a) remap[a] = -1;
-    for (int i = 0; i < n; ++i) remap[agg[i]] = 1;
+    for (int i = 0; i < n; ++i)
+      if (agg[i] >= 0) remap[agg[i]] = 1;
     int m = 0;
     for (int a = 0; a < n_agg; ++a)
       if (remap[a] == 1) remap[a] = m++;
     for (int a = 0; a < n_agg; ++a) size[a] = 0;
-    for (int i = 0; i < n; ++i) { agg[i] = remap[agg[i]]; size[agg[i]]++; }
+    for (int i = 0; i < n; ++i)
+      if (agg[i] >= 0) { agg[i] = remap[agg[i]]; size[agg[i]]++; }
     n_agg = m;
     if (m < 2) break;
     int small = -1;

@@ -41,8 +41,9 @@ struct Level {
   DevBuf<double> coef, lmax, wdev;
   // smoothed-aggregation provenance (exported for parity tests)
   DevBuf<int> agg, sptr, scol;
-  int n_agg = 0;
-  Bsr Tm;  // tentative prolongation
+  int n_agg = 0, n_dropped = 0;  // n_dropped: unaggregated (-1) nodes
+  Bsr Tm;                        // tentative prolongation (BSR)
+  DevBuf<double> Tnode;          // its blocks indexed by node (zero when unaggregated)
   DevBuf<double> rho;
   bool lattice() const { return opkind != OP_BSR; }
 };
@@ -55,7 +56,8 @@ struct Hierarchy {
   DenseInverse coarse;
   std::vector<int> provenance;  // 0 geometric, 1 algebraic (per level)
   std::vector<std::string> flags;
-  RedSlot red;  // scratch reduction for setup
+  bool drop_isolated = false;  // SA: leave strength-isolated nodes unaggregated (extension)
+  RedSlot red;                 // scratch reduction for setup
   int last() const { return (int)lv.size() - 1; }
   // fused-kernel V-cycle applies (point Jacobi, at least one pre-sweep)
   bool fused() const { return sm.kind == SM_JACOBI && n_pre > 0; }

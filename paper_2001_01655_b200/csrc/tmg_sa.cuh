@@ -4,9 +4,33 @@
 // the device.  The host only reads back a handful of integers per level
 // (aggregate counts, overflow/error flags) to size the next allocations.
 #pragma once
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "tmg_gmg.cuh"
 
 namespace tmg {
+
+// TMG_VERBOSE=1: per-phase setup timings on stderr (synchronises the stream).
+struct PhaseLog {
+  bool on = false;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseLog(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("TMG_VERBOSE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, long long a = -1) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tmg] %-28s %9.3f ms  %lld\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count(), a);
+    t0 = t;
+  }
+};
 
 __global__ void k_sqrt_to(const double* __restrict__ v2, double* __restrict__ out) { *out = sqrt(*v2); }
 __global__ void k_clamp_agg(int* __restrict__ agg, int n, int n_reg) {
@@ -157,8 +181,8 @@ inline void bsr_spgemm(const Bsr& X, const Bsr& Y, Bsr& Cm, cudaStream_t s) {
 }
 
 // aggregate_nodes + _merge_small_aggregates on the strength graph of A
-inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, Level& l, std::vector<std::string>& flags,
-                            cudaStream_t s) {
+inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool drop_isolated, Level& l,
+                            std::vector<std::string>& flags, cudaStream_t s) {
   const int n = A.nrows;
   DevBuf<double> md;
   md.alloc(n, s);
@@ -197,7 +221,10 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, Level& 
     int* a4 = flag.get();
     int* a5 = rounds.get();
     void* args[] = {(void*)&a0, (void*)&a1, (void*)&n, (void*)&a3, (void*)&a4, (void*)&a5};
+    PhaseLog lg(s);
+    lg.mark("  strength graph (nnz)", snnz);
     TMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis, blocks, TPB, args, 0, s));
+    if (lg.on) lg.mark("  LFMIS (rounds)", read_int(rounds.get(), s));
   }
   DevBuf<int> isroot, rank, agg1, ptr, isoflag, isorank;
   isroot.alloc(n + 1, s); rank.alloc(n + 1, s); agg1.alloc(n, s); ptr.alloc(n, s);
@@ -224,11 +251,14 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, Level& 
     forced = true;
     flags.push_back("forced_pairwise_aggregation");
   } else if (U > 0) {
-    k_assign_isolated<<<grid_for(n), TPB, 0, s>>>(n, isorank.get(), n_agg, l.agg.get());
-    note_launch();
-    n_agg += U;
+    if (!drop_isolated) {
+      k_assign_isolated<<<grid_for(n), TPB, 0, s>>>(n, isorank.get(), n_agg, l.agg.get());
+      note_launch();
+      n_agg += U;
+    }
     flags.push_back("isolated_nodes");
   }
+  l.n_dropped = (forced || !drop_isolated) ? 0 : U;
   // _merge_small_aggregates
   const int min_size = std::max(2, (nvec + bs - 1) / bs);
   DevBuf<int> size;
@@ -242,7 +272,7 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, Level& 
   int n_small = 0;
   for (int a = 0; a < n_agg; ++a) n_small += hsize[a] < min_size ? 1 : 0;
   if (n_small > 0) {
-    if (!forced && min_size == 2 && n_small == U) {
+    if (!forced && !drop_isolated && min_size == 2 && n_small == U) {
       // the small aggregates are exactly the isolated singletons: they have no
       // strong neighbour, so the index-neighbour fallback folds each into the
       // last regular aggregate (multigrid.py:457-467)
@@ -291,28 +321,37 @@ inline void tentative_level(Level& l, const double* B, int n, int bs, int nv, De
   TMG_CUDA(cudaMemcpyAsync(woff.get(), hoff.data(), (na + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
   DevBuf<double> work;
   work.alloc(std::max<long long>(hoff[na], 1), s);
-  Bsr& T = l.Tm;
-  T.nrows = n;
-  T.ncols = na;
-  T.R = bs;
-  T.C = nv;
-  T.nnzb = n;
-  T.rowptr.alloc(n + 1, s);
-  k_iota<<<grid_for(n + 1), TPB, 0, s>>>(T.rowptr.get(), n + 1);
-  T.col.alloc(n, s);
-  TMG_CUDA(cudaMemcpyAsync(T.col.get(), l.agg.get(), n * sizeof(int), cudaMemcpyDeviceToDevice, s));
-  T.val.alloc((long long)n * bs * nv, s);
+  // node-indexed blocks (zero for unaggregated nodes), then the BSR view
+  l.Tnode.alloc((long long)n * bs * nv, s);
+  l.Tnode.zero(s);
   Bc.alloc((long long)na * nv * nv, s);
   DevBuf<int> bad;
   bad.alloc(1, s);
   bad.zero(s);
-  k_tentative_qr<<<na, 128, 0, s>>>(offs.get(), members.get(), bs, nv, B, work.get(), woff.get(), T.val.get(),
-                                    Bc.get(), bad.get());
+  // radix sort puts the unaggregated (-1) nodes first: skip them
+  k_tentative_qr<<<na, 128, 0, s>>>(offs.get(), members.get() + l.n_dropped, bs, nv, B, work.get(), woff.get(),
+                                    l.Tnode.get(), Bc.get(), bad.get());
   note_launch(4);
   const int hbad = read_int(bad.get(), s);
   if (hbad)
     throw Error(-1, "aggregate with " + std::to_string(hbad) + " dofs cannot carry " + std::to_string(nv) +
                         " candidates");
+  Bsr& T = l.Tm;
+  T.nrows = n;
+  T.ncols = na;
+  T.R = bs;
+  T.C = nv;
+  DevBuf<int> cnt;
+  cnt.alloc(n + 1, s);
+  cnt.zero(s);
+  k_flag_nonneg<<<grid_for(n), TPB, 0, s>>>(l.agg.get(), n, cnt.get());
+  rowptr_from_counts(cnt, T.rowptr, n, s);
+  T.nnzb = n - l.n_dropped;
+  T.col.alloc(std::max<long long>(T.nnzb, 1), s);
+  T.val.alloc(std::max<long long>(T.nnzb, 1) * bs * nv, s);
+  k_compact_T<<<grid_for(n), TPB, 0, s>>>(n, l.agg.get(), T.rowptr.get(), l.Tnode.get(), bs * nv, T.col.get(),
+                                          T.val.get());
+  note_launch(2);
   TMG_CUDA(cudaGetLastError());
 }
 
@@ -347,7 +386,7 @@ template <int BS, int NV>
 void smooth_p_typed(const Bsr& A, const Level& l, const double* dinv, Bsr& P, cudaStream_t s) {
   bsr_spgemm(A, l.Tm, P, s);
   k_p_from_at<BS, NV><<<grid_for(P.nrows), TPB, 0, s>>>(P.nrows, P.rowptr.get(), P.col.get(), P.val.get(),
-                                                        l.agg.get(), l.Tm.val.get(), dinv, l.rho.get());
+                                                        l.agg.get(), l.Tnode.get(), dinv, l.rho.get());
   note_launch();
   TMG_CUDA(cudaGetLastError());
 }
@@ -369,17 +408,21 @@ void sa_levels(Hierarchy& H, const double* B_dev, int nvec, int bs, long long co
   DevBuf<double> Bcur;  // candidates of the current level (device)
   const double* B = B_dev;
   int added = 0;
+  PhaseLog log(s);
   while (H.lv.back()->ndof > coarse_max_dofs && added < max_levels) {
     Level& l = *H.lv.back();
+    log.mark("sa level start (ndof)", l.ndof);
     Bsr Atmp;
     const Bsr* A = &l.Ab;
     if (l.lattice()) {
       lattice_to_bsr<DIM>(l, Atmp, s);
       A = &Atmp;
+      log.mark("lattice->bsr (nnzb)", Atmp.nnzb);
     }
     const int n = A->nrows;
     std::vector<std::string> f;
-    aggregate_level(*A, beta, bs, nvec, l, f, s);
+    aggregate_level(*A, beta, bs, nvec, H.drop_isolated, l, f, s);
+    log.mark("strength+aggregation (n_agg)", l.n_agg);
     H.flags.insert(H.flags.end(), f.begin(), f.end());
     if ((long long)l.n_agg * nvec >= l.ndof) {
       H.flags.push_back("aggregation_stalled");
@@ -387,6 +430,7 @@ void sa_levels(Hierarchy& H, const double* B_dev, int nvec, int bs, long long co
     }
     DevBuf<double> Bc;
     tentative_level(l, B, n, bs, nvec, Bc, s);
+    log.mark("tentative QR");
     // D^-1 of this level and omega
     DevBuf<double> d, dinv;
     DevBuf<unsigned> bad;
@@ -395,14 +439,18 @@ void sa_levels(Hierarchy& H, const double* B_dev, int nvec, int bs, long long co
     k_recip<<<grid_for(l.ndof), TPB, 0, s>>>(d.get(), dinv.get(), nullptr, l.ndof);
     note_launch(2);
     spectral_radius(H, *A, bs, dinv.get(), v0, l.ndof, l.rho, s);
+    log.mark("spectral radius");
     smooth_p(*A, l, dinv.get(), bs, nvec, l.P, s);
+    log.mark("smoothed P (nnzb)", l.P.nnzb);
     bsr_transpose(l.P, l.Pt, s);
     Bsr AP;
     bsr_spgemm(*A, l.P, AP, s);
+    log.mark("P^T, A*P (nnzb)", AP.nnzb);
     auto c = std::make_unique<Level>();
     c->opkind = OP_BSR;
     c->bs = nvec;
     bsr_spgemm(l.Pt, AP, c->Ab, s);
+    log.mark("P^T*(A*P) (nnzb)", c->Ab.nnzb);
     c->ndof = (long long)l.n_agg * nvec;
     l.xfer = XF_SPARSE;
     H.provenance.back() = 1;
@@ -418,8 +466,9 @@ void sa_levels(Hierarchy& H, const double* B_dev, int nvec, int bs, long long co
 template <int DIM>
 std::unique_ptr<Hierarchy> build_sa_amg(const Operator& K, const double* B_dev, int nvec, long long coarse_max_dofs,
                                         double beta, const double* v0, const SmootherCfg& sm, int n_pre, int n_post,
-                                        cudaStream_t s) {
+                                        bool drop_isolated, cudaStream_t s) {
   auto H = new_hierarchy<DIM>(sm, n_pre, n_post, s);
+  H->drop_isolated = drop_isolated;
   const int bs = nvec == 3 ? 2 : nvec == 6 ? 3 : 1;
   TMG_REQUIRE(bs == DIM, "near-nullspace columns do not match the mesh dimension (3 in 2D, 6 in 3D)");
   H->lv.push_back(fine_level<DIM>(K));
@@ -441,8 +490,9 @@ template <int DIM>
 std::unique_ptr<Hierarchy> build_hybrid(const Operator& K, int n_geo, const double* B_coarse, int nvec,
                                         long long coarse_max_dofs, double beta, const double* v0,
                                         const SmootherCfg& sm, int n_pre, int n_post, long long expect_sa_ndof,
-                                        cudaStream_t s) {
+                                        bool drop_isolated, cudaStream_t s) {
   auto H = new_hierarchy<DIM>(sm, n_pre, n_post, s);
+  H->drop_isolated = drop_isolated;
   H->lv.push_back(fine_level<DIM>(K));
   H->provenance.push_back(0);
   std::vector<std::array<int, 3>> plan;

@@ -244,10 +244,12 @@ def _host_or_device(a):
 
 
 def build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0,
-                 beta=DEFAULT_STRENGTH_BETA, stream=None, v0=None):
+                 beta=DEFAULT_STRENGTH_BETA, stream=None, v0=None, isolated="merge"):
     """Smoothed-aggregation hierarchy built on the device (multigrid.py:555).
     EXTENSION: beta (the reference fixes 0.003); v0 overrides the power-method start
-    vector default_rng(seed).standard_normal(n) (e.g. a device-resident copy)."""
+    vector default_rng(seed).standard_normal(n) (e.g. a device-resident copy);
+    isolated="drop" leaves strength-isolated nodes unaggregated instead of folding
+    them into one aggregate (reference: "merge", multigrid.py:418-423/457-467)."""
     smoother = smoother or SmootherConfig()
     if smoother.kind not in SMOOTHER_KINDS:
         raise ValueError("unknown smoother kind %r" % smoother.kind)
@@ -258,10 +260,18 @@ def build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother=None, n_pre=1, n_p
     h = C.c_void_p()
     _lib.check(_lib.load().tmg_sa_amg_build(K.handle, pB, B.shape[1], int(coarse_max_dofs),
                                             float(beta), pv, C.byref(smoother.desc()),
-                                            int(n_pre), int(n_post), stream_ptr(stream), C.byref(h)))
+                                            int(n_pre), int(n_post), isolated_mode(isolated),
+                                            stream_ptr(stream), C.byref(h)))
     H = MgHierarchy(h, K, smoother, n_pre, n_post)
     H.flags = H.device_flags()
     return H
+
+
+def isolated_mode(isolated):
+    """C-ABI code of the isolated-node policy ("merge" = reference, "drop")."""
+    if isolated not in ("merge", "drop"):
+        raise ValueError("isolated must be 'merge' or 'drop', got %r" % (isolated,))
+    return 0 if isolated == "merge" else 1
 
 
 def hybrid_plan(mesh, n_geo, coarse_max_dofs):
@@ -281,12 +291,13 @@ def hybrid_plan(mesh, n_geo, coarse_max_dofs):
 
 
 def build_hybrid(mesh, K, near_nullspace, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_post=1,
-                 seed=0, beta=DEFAULT_STRENGTH_BETA, stream=None):
+                 seed=0, beta=DEFAULT_STRENGTH_BETA, stream=None, isolated="merge"):
     """Geometric transfers on the finest n_geo levels, SA below (multigrid.py:573)."""
     from .mesh import StructuredMesh, rigid_body_modes
     smoother = smoother or SmootherConfig()
     if n_geo <= 0:
-        return build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother, n_pre, n_post, seed, beta, stream)
+        return build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother, n_pre, n_post, seed, beta, stream,
+                            isolated=isolated)
     dims, sizes, _ = hybrid_plan(mesh, n_geo, coarse_max_dofs)
     Bc = np.ascontiguousarray(rigid_body_modes(StructuredMesh(dims, sizes)))
     v0 = _start_vector(Bc.shape[0], seed)
@@ -294,7 +305,7 @@ def build_hybrid(mesh, K, near_nullspace, n_geo, coarse_max_dofs, smoother=None,
     _lib.check(_lib.load().tmg_hybrid_build(K.handle, int(n_geo), Bc.ctypes.data, Bc.shape[0], Bc.shape[1],
                                             int(coarse_max_dofs), float(beta), v0.ctypes.data,
                                             C.byref(smoother.desc()), int(n_pre), int(n_post),
-                                            stream_ptr(stream), C.byref(h)))
+                                            isolated_mode(isolated), stream_ptr(stream), C.byref(h)))
     H = MgHierarchy(h, K, smoother, n_pre, n_post)
     H.flags = H.device_flags()
     return H

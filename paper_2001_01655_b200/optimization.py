@@ -33,6 +33,7 @@ class SolverHarness:
     n_post: int = 1
     max_levels: int | None = None
     beta: float = DEFAULT_STRENGTH_BETA
+    isolated: str = "merge"
 
     @property
     def near_nullspace(self):
@@ -48,10 +49,12 @@ class SolverHarness:
                           self.max_levels)
         elif self.strategy == "amg":
             h = build_sa_amg(K, self.near_nullspace, self.coarse_max_dofs, self.smoother, self.n_pre,
-                             self.n_post, seed=self.seed, beta=self.beta)
+                             self.n_post, seed=self.seed, beta=self.beta,
+                             isolated=self.isolated)
         elif self.strategy == "hybrid":
             h = build_hybrid(self.mesh, K, self.near_nullspace, self.n_geo, self.coarse_max_dofs,
-                             self.smoother, self.n_pre, self.n_post, seed=self.seed, beta=self.beta)
+                             self.smoother, self.n_pre, self.n_post, seed=self.seed, beta=self.beta,
+                             isolated=self.isolated)
         else:
             raise ValueError("unknown preconditioner strategy %r" % self.strategy)
         torch_sync()

@@ -25,8 +25,9 @@ def clamped(dims, seed, void=True):
     return cantilever(dims, seed, void=void)
 
 
-def oracle_sa(g, Kref, fixed, bound, beta, sm, n_pre=2, n_post=2):
-    return O.build_sa_amg(Kref, O.rigid_body_modes(g, fixed), bound, sm, n_pre, n_post, beta=beta)
+def oracle_sa(g, Kref, fixed, bound, beta, sm, n_pre=2, n_post=2, isolated="merge"):
+    return O.build_sa_amg(Kref, O.rigid_body_modes(g, fixed), bound, sm, n_pre, n_post, beta=beta,
+                          isolated=isolated)
 
 
 def spdiff(A, B):
@@ -34,12 +35,16 @@ def spdiff(A, B):
     return (np.max(np.abs(D.data)) if D.nnz else 0.0) / max(np.max(np.abs(sp.csr_matrix(B).data)), 1e-300)
 
 
-@pytest.mark.parametrize("dims,beta", [((12, 8), 0.08), ((24, 12), 0.003), ((6, 4, 4), 0.08), ((8, 4, 4), 0.003)])
-def test_sa_setup_pieces(dims, beta):
+@pytest.mark.parametrize("dims,beta,isolated", [((12, 8), 0.08, "merge"), ((24, 12), 0.003, "merge"),
+                                                ((6, 4, 4), 0.08, "merge"), ((8, 4, 4), 0.003, "merge"),
+                                                ((24, 12), 0.08, "drop"), ((8, 4, 4), 0.0064, "drop")])
+def test_sa_setup_pieces(dims, beta, isolated):
     mesh, g, bc, rho, E, K, Kref = clamped(dims, 4)
     B = T.rigid_body_modes(mesh, bc.fixed_dofs)
-    h = T.build_sa_amg(K, B, 40, T.SmootherConfig(weight=0.6), 2, 2, beta=beta)
-    ho = oracle_sa(g, Kref, bc.fixed_dofs, 40, beta, O.Smoother(weight=0.6))
+    h = T.build_sa_amg(K, B, 40, T.SmootherConfig(weight=0.6), 2, 2, beta=beta, isolated=isolated)
+    ho = oracle_sa(g, Kref, bc.fixed_dofs, 40, beta, O.Smoother(weight=0.6), isolated=isolated)
+    if isolated == "drop":  # the case must exercise the extension: unaggregated nodes exist
+        assert (ho.levels[0].aggregates < 0).any()
     assert [lv.size for lv in h.levels] == [lv.A.shape[0] for lv in ho.levels]
     assert sorted(set(h.flags)) == sorted(set(ho.flags))
     assert all(lv.provenance == "algebraic" for lv in h.levels)
@@ -74,12 +79,13 @@ def test_sa_forced_pairwise_odd():
     assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-9
 
 
-@pytest.mark.parametrize("dims,beta", [((32, 16), 0.08), ((10, 6, 6), 0.08)])
-def test_amg_pcg_matches_oracle(dims, beta):
+@pytest.mark.parametrize("dims,beta,isolated", [((32, 16), 0.08, "merge"), ((10, 6, 6), 0.08, "merge"),
+                                                ((48, 16), 0.08, "drop"), ((12, 6, 6), 0.0064, "drop")])
+def test_amg_pcg_matches_oracle(dims, beta, isolated):
     mesh, g, bc, rho, E, K, Kref = clamped(dims, 7)
     B = T.rigid_body_modes(mesh, bc.fixed_dofs)
-    h = T.build_sa_amg(K, B, 60, T.SmootherConfig(weight=0.6), 2, 2, beta=beta)
-    ho = oracle_sa(g, Kref, bc.fixed_dofs, 60, beta, O.Smoother(weight=0.6))
+    h = T.build_sa_amg(K, B, 60, T.SmootherConfig(weight=0.6), 2, 2, beta=beta, isolated=isolated)
+    ho = oracle_sa(g, Kref, bc.fixed_dofs, 60, beta, O.Smoother(weight=0.6), isolated=isolated)
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
     assert rec.converged and reco.converged
@@ -133,3 +139,22 @@ def test_sa_validates_nullspace_shape():
     mesh, g, bc, rho, E, K, Kref = cantilever((4, 2), 1)
     with pytest.raises(ValueError):
         T.build_sa_amg(K, np.ones(g.n_dofs), 20)
+    with pytest.raises(ValueError):
+        T.build_sa_amg(K, T.rigid_body_modes(mesh, bc.fixed_dofs), 20, isolated="keep")
+
+
+# Drop-mode cases avoid 3D aggregates of two 3-dof nodes: their 6x6 rigid-mode block
+# has rank 5 (rotation about the joining axis vanishes) -- the rank-deficient
+# situation described above test_hybrid_matches_oracle.
+def test_hybrid_drop_matches_oracle():
+    mesh, g, bc, rho, E, K, Kref = cantilever((64, 32), 6, void=True)
+    sm = T.SmootherConfig(kind="chebyshev", weight=1.0)
+    B = T.rigid_body_modes(mesh, bc.fixed_dofs)
+    h = T.build_hybrid(mesh, K, B, 1, 60, sm, 1, 1, beta=0.08, isolated="drop")
+    ho = O.build_hybrid(g, Kref, O.rigid_body_modes(g, bc.fixed_dofs), 1, 60, O.Smoother(kind="chebyshev"),
+                        1, 1, beta=0.08, isolated="drop")
+    assert [lv.size for lv in h.levels] == [lv.A.shape[0] for lv in ho.levels]
+    for k, lv in enumerate(ho.levels):
+        assert spdiff(h.level_matrix(k), lv.A) <= 1e-11, k
+    b = np.random.default_rng(3).standard_normal(g.n_dofs)
+    assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-9
