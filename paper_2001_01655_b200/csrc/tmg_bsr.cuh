@@ -2,8 +2,11 @@
 // SA-AMG coarse operators (nvec x nvec blocks), prolongations P (bs x nvec) and
 // restrictions P^T (nvec x bs).  Column indices are sorted within each block row
 // (the reference's scipy CSR matrices are canonical, multigrid.py:262), blocks are
-// row-major.  One thread per block row; the R outputs of a row stay in registers.
+// row-major.  Row kernels give each block row a group of 2^gshift lanes; the R
+// outputs of a row stay in registers.
 #pragma once
+#include <algorithm>
+
 #include "tmg_ops.cuh"
 
 namespace tmg {
@@ -23,40 +26,74 @@ struct BsrView {
   const int* __restrict__ col;
   const double* __restrict__ val;
   int nrows;
+  int gshift;  // 2^gshift lanes cooperate on one block row (row kernels below)
 };
+// Lanes per block row: the largest power of two <= half the mean blocks per row
+// (<= 32).  The coarse Galerkin levels carry 15-60 blocks per row, where one
+// thread per row is a serial latency chain; the fine-level P (3 blocks per row)
+// keeps 1-2 lanes.  Runtime value: the xor-butterfly below never leaves its
+// aligned group, so no template instantiation per group size is needed.
+inline int bsr_gshift(int nrows, long long nnzb) {
+  const double avg = nrows > 0 ? double(nnzb) / nrows : 1.0;
+  int g = 0;
+  while (g < 5 && double(2 << g) <= avg) ++g;
+  return g;
+}
 template <int R, int C>
 inline BsrView<R, C> view(const Bsr& m) {
-  return BsrView<R, C>{m.rowptr.get(), m.col.get(), m.val.get(), m.nrows};
+  return BsrView<R, C>{m.rowptr.get(), m.col.get(), m.val.get(), m.nrows, bsr_gshift(m.nrows, m.nnzb)};
+}
+// grid of a row kernel on m (threads = rows << gshift)
+inline unsigned bsr_grid(const Bsr& m) {
+  const long long t = (long long)m.nrows << bsr_gshift(m.nrows, m.nnzb);
+  return (unsigned)std::max<long long>(1, (t + TPB - 1) / TPB);
 }
 
-// y_row = sum_j A_rj x_j  (row of R outputs)
+// Row handled by this thread's lane group, and the lane within the group.
 template <int R, int C>
-__device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, const double* __restrict__ x,
+__device__ __forceinline__ int bsr_row_id(const BsrView<R, C>& A, int& lane) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  lane = (int)(t & ((1 << A.gshift) - 1));
+  return (int)(t >> A.gshift);
+}
+
+// y_row = sum_j A_rj x_j (row of R outputs), lanes of a group stride over the
+// row's blocks and combine with an xor butterfly: every lane of the group ends
+// with the full sums.  Must be reached by all lanes of the warp (rows past the
+// end contribute zeros).
+template <int R, int C>
+__device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lane, const double* __restrict__ x,
                                         double out[R]) {
 #pragma unroll
   for (int a = 0; a < R; ++a) out[a] = 0.0;
-  const int e = A.rowptr[row + 1];
-  for (int p = A.rowptr[row]; p < e; ++p) {
-    const int j = A.col[p];
-    double xv[C];
+  if (row < A.nrows) {
+    const int e = A.rowptr[row + 1];
+    for (int p = A.rowptr[row] + lane; p < e; p += (1 << A.gshift)) {
+      const int j = A.col[p];
+      double xv[C];
 #pragma unroll
-    for (int b = 0; b < C; ++b) xv[b] = __ldg(x + (long long)j * C + b);
-    const double* blk = A.val + (long long)p * R * C;
+      for (int b = 0; b < C; ++b) xv[b] = __ldg(x + (long long)j * C + b);
+      const double* blk = A.val + (long long)p * R * C;
 #pragma unroll
-    for (int a = 0; a < R; ++a)
+      for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int b = 0; b < C; ++b) out[a] += __ldg(blk + a * C + b) * xv[b];
+        for (int b = 0; b < C; ++b) out[a] += __ldg(blk + a * C + b) * xv[b];
+    }
   }
+  for (int off = (1 << A.gshift) >> 1; off > 0; off >>= 1)
+#pragma unroll
+    for (int a = 0; a < R; ++a) out[a] += __shfl_xor_sync(0xffffffffu, out[a], off);
 }
 
 // y = A x (+ y if accumulate)
 template <int R, int C>
 __global__ void __launch_bounds__(TPB) k_bsr_apply(BsrView<R, C> A, const double* __restrict__ x,
                                                    double* __restrict__ y, int accumulate) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.nrows) return;
+  int lane;
+  const int row = bsr_row_id(A, lane);
   double out[R];
-  bsr_row<R, C>(A, row, x, out);
+  bsr_row<R, C>(A, row, lane, x, out);
+  if (row >= A.nrows || lane != 0) return;
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     const long long i = (long long)row * R + a;
@@ -70,10 +107,11 @@ template <int R, int C>
 __global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const double* __restrict__ r,
                                                       double* __restrict__ bc, const double* __restrict__ dinvc,
                                                       const double* __restrict__ wp, double* __restrict__ xc) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= Pt.nrows) return;
+  int lane;
+  const int row = bsr_row_id(Pt, lane);
   double out[R];
-  bsr_row<R, C>(Pt, row, r, out);
+  bsr_row<R, C>(Pt, row, lane, r, out);
+  if (row >= Pt.nrows || lane != 0) return;
   const double w = xc ? *wp : 0.0;
 #pragma unroll
   for (int a = 0; a < R; ++a) {
@@ -87,10 +125,11 @@ __global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const do
 template <int R>
 __global__ void __launch_bounds__(TPB) k_bsr_residual(BsrView<R, R> A, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ r) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.nrows) return;
+  int lane;
+  const int row = bsr_row_id(A, lane);
   double out[R];
-  bsr_row<R, R>(A, row, x, out);
+  bsr_row<R, R>(A, row, lane, x, out);
+  if (row >= A.nrows || lane != 0) return;
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     const long long i = (long long)row * R + a;
@@ -103,12 +142,13 @@ template <int R, bool DOT>
 __global__ void __launch_bounds__(TPB) k_bsr_jacobi(BsrView<R, R> A, const double* __restrict__ x,
                                                     const double* __restrict__ b, const double* __restrict__ dinv,
                                                     const double* __restrict__ wp, double* __restrict__ xo, Red red) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  int lane;
+  const int row = bsr_row_id(A, lane);
+  double out[R];
+  bsr_row<R, R>(A, row, lane, x, out);
   double v = 0.0;
-  if (row < A.nrows) {
+  if (row < A.nrows && lane == 0) {
     const double w = *wp;
-    double out[R];
-    bsr_row<R, R>(A, row, x, out);
 #pragma unroll
     for (int a = 0; a < R; ++a) {
       const long long i = (long long)row * R + a;
@@ -136,11 +176,12 @@ __global__ void __launch_bounds__(TPB) k_bsr_cheb(BsrView<R, R> A, const double*
                                                   const double* __restrict__ pn, const double* __restrict__ coef,
                                                   int step, int x_zero, double* __restrict__ x,
                                                   double* __restrict__ ro) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.nrows) return;
+  int lane;
+  const int row = bsr_row_id(A, lane);
   const double alpha = coef[2 * step];
   double out[R];
-  bsr_row<R, R>(A, row, pn, out);
+  bsr_row<R, R>(A, row, lane, pn, out);
+  if (row >= A.nrows || lane != 0) return;
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     const long long i = (long long)row * R + a;
@@ -154,10 +195,11 @@ template <int R>
 __global__ void __launch_bounds__(TPB) k_bsr_apply_sym(BsrView<R, R> A, const double* __restrict__ v,
                                                        const double* __restrict__ ds, double* __restrict__ tmp,
                                                        double* __restrict__ y) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.nrows) return;
+  int lane;
+  const int row = bsr_row_id(A, lane);
   double out[R];
-  bsr_row<R, R>(A, row, tmp, out);
+  bsr_row<R, R>(A, row, lane, tmp, out);
+  if (row >= A.nrows || lane != 0) return;
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     const long long i = (long long)row * R + a;

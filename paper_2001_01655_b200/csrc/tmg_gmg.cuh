@@ -88,7 +88,7 @@ void with_bsr(const Level& l, F&& f) {
 }
 // launch configuration of a node kernel on level l with operator `o` in scope
 #define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), decltype(o)::SMEM_BYTES
-#define TMG_ROW_LAUNCH(l) grid_for((l).Ab.nrows), TPB, 0
+#define TMG_ROW_LAUNCH(l) bsr_grid((l).Ab), TPB, 0
 
 template <int DIM>
 void lvl_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
@@ -394,7 +394,7 @@ void xfer_restrict(Hierarchy& H, int k, const double* r, double* xc_first, cudaS
                                                                        xc_first);
   } else {
     TMG_BSR_RECT_DISPATCH(l.Pt.R, l.Pt.C,
-                          k_bsr_restrict<RR, CC><<<grid_for(l.Pt.nrows), TPB, 0, s>>>(
+                          k_bsr_restrict<RR, CC><<<bsr_grid(l.Pt), TPB, 0, s>>>(
                               view<RR, CC>(l.Pt), r, c.b.get(), c.dinv.get(), c.wdev.get(), xc_first))
   }
   note_launch();
@@ -407,7 +407,7 @@ void xfer_prolong_add(Hierarchy& H, int k, double* x, cudaStream_t s) {
     k_prolong_add<DIM><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(l.T, c.x.get(), x);
   } else {
     TMG_BSR_RECT_DISPATCH(l.P.R, l.P.C,
-                          k_bsr_apply<RR, CC><<<grid_for(l.P.nrows), TPB, 0, s>>>(view<RR, CC>(l.P), c.x.get(), x, 1))
+                          k_bsr_apply<RR, CC><<<bsr_grid(l.P), TPB, 0, s>>>(view<RR, CC>(l.P), c.x.get(), x, 1))
   }
   note_launch();
 }

@@ -368,7 +368,7 @@ inline void spectral_radius(Hierarchy& H, const Bsr& A, int bs, const double* di
     rn.result = nrm.get();
     k_dot<<<gr, TPB, 0, s>>>(v.get(), v.get(), nd, rn);
     k_div_sqrt<<<g, TPB, 0, s>>>(v.get(), nrm.get(), nd);
-    TMG_BSR_SQUARE_DISPATCH(bs, k_bsr_apply<RR, RR><<<grid_for(A.nrows), TPB, 0, s>>>(view<RR, RR>(A), v.get(),
+    TMG_BSR_SQUARE_DISPATCH(bs, k_bsr_apply<RR, RR><<<bsr_grid(A), TPB, 0, s>>>(view<RR, RR>(A), v.get(),
                                                                                        t.get(), 0))
     k_vmul<<<g, TPB, 0, s>>>(dinv, t.get(), v.get(), nd);
     note_launch(4);

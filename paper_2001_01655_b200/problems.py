@@ -128,7 +128,8 @@ def config_1(seed=1655):
                     solvers=[dict(strategy="gmg", levels=5, smoother="weighted_jacobi", weight=0.6,
                                   n_pre=2, n_post=2, safeguard=1.8, max_iterations=2000),
                              dict(strategy="amg", coarse_max_dofs=499, beta=BETA, isolated="drop",
-                                  smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2)])
+                                  smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2,
+                                  max_iterations=2000)])
 
 
 def config_2(seed=2001):
