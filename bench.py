@@ -53,6 +53,20 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def replica_throughput(local_ms, local_work, world, device):
+    """Whole-job throughput of N independent replicas: every rank did the same
+    work; the job took as long as the slowest rank (max over ranks of the
+    device-timed region).  Returns (max_ms, units/s)."""
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.barrier()
+        t = torch.tensor([local_ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        local_ms = float(t.item())
+    return local_ms, world * local_work / (local_ms / 1e3)
+
+
 def config_dict(w, args, world):
     from paper_2001_01655_b200 import problems
     return {"workload": w.name, "config_index": args.config, "ndof": int(w.ndof),
@@ -115,6 +129,12 @@ class Clocks:
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 def oracle_sample(w, leg, iters):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):  # "cores": 1 is what the line claims
+        return _oracle_sample(w, leg, iters)
+
+
+def _oracle_sample(w, leg, iters):
     from oracle import topomg_oracle as O
     from paper_2001_01655_b200 import problems
     g = O.make_grid(w.mesh.dims)
@@ -295,12 +315,7 @@ def run_b200(args, rank, world, local):
             total_ms += e0.elapsed_time(e1)
             total_work += wk
     launches = L.tmg_launch_count() - launches0
-    if world > 1:
-        torch.distributed.barrier()
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * total_work / (total_ms / 1e3)
+    total_ms, value = replica_throughput(total_ms, total_work, world, "cuda")
     roof = roofline(args, w, state, L)
     e2e = e2e_run(args, w, runners, L, law)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
