@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--cpu-sample-iters", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--iters-cap", type=int, default=0,
+                   help="profiling only: cap every leg's PCG iterations (ncu launch lists)")
     return p.parse_args()
 
 
@@ -267,6 +269,9 @@ def run_b200(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = problems.CONFIGS[args.config]()
     runners = [LegRunner(w, leg) for leg in w.solvers]
+    if args.iters_cap > 0:
+        for lr in runners:
+            lr.maxit = min(lr.maxit, args.iters_cap)
     L = _lib.load()
     law = T.SimpLaw(penalty=problems.PENAL, e_min_ratio=problems.EMIN)
     rho_d = as_dev(w.rho)
@@ -366,7 +371,7 @@ def roofline(args, w, state, L):
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "bytes_per_launch": bytes_launch, "launch_us": ms.value * 1e3,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-            "timing": "CUDA events around 50 back-to-back launches on the launching stream",
+            "timing": "CUDA events around one replay of a CUDA graph of 50 back-to-back launches",
             "note": "working set %.1f MB vs 126 MB L2" % (bytes_launch / 1e6)}
 
 

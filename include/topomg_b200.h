@@ -154,11 +154,14 @@ int tmg_hierarchy_level_apply(tmg_hierarchy* h, int32_t level, const double* x_d
 /* Chebyshev eigenvalue estimate of a level (NaN unless the smoother is chebyshev). */
 int tmg_hierarchy_level_lmax(tmg_hierarchy* h, int32_t level, double* lmax_host, void* stream);
 
-/* Average device time (ms, CUDA events on `stream`) of one smoother sweep kernel of
- * a level (weighted/block Jacobi sweep or one Chebyshev step), over `reps` launches.
+/* Average device time (ms) of one smoother sweep kernel of a level (weighted/block
+ * Jacobi sweep or one Chebyshev step): `reps` launches captured into one CUDA graph
+ * and timed with CUDA events as one replay (back to back, as inside the PCG graph).
  * Used by bench.py for the roofline of the dominant kernel. */
 int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, double* ms_host,
                                 void* stream);
+/* Same for one V-cycle started at `level` (diagnostics: per-level cost split). */
+int tmg_hierarchy_time_vcycle(tmg_hierarchy* h, int32_t level, int32_t reps, double* ms_host, void* stream);
 
 /* Preconditioned CG (extension; krylov.py:134 is the reference's GMRES entry).
  * h may be NULL (unpreconditioned).  x_dev holds x0 on entry when use_x0 != 0

@@ -36,6 +36,7 @@ namespace cg = cooperative_groups;
 // ----------------------------------------------------------------------------
 template <int DIM, class Op>
 __global__ void k_lattice_bsr_count(const __grid_constant__ Op op, int* __restrict__ cnt) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   if (!active) return;
   int c = 0;
@@ -47,6 +48,7 @@ __global__ void k_lattice_bsr_count(const __grid_constant__ Op op, int* __restri
 template <int DIM, class Op>
 __global__ void k_lattice_bsr_fill(const __grid_constant__ Op op, const int* __restrict__ rowptr,
                                    int* __restrict__ col, double* __restrict__ val) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   if (!active) return;
   int p = rowptr[node];
@@ -78,6 +80,7 @@ __device__ __forceinline__ double block_sq(const double* __restrict__ blk) {
 }
 template <int R>
 __global__ void k_strength_diag(BsrView<R, R> A, double* __restrict__ md, unsigned* __restrict__ bad) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.nrows) return;
   double m = 0.0;
@@ -89,6 +92,7 @@ __global__ void k_strength_diag(BsrView<R, R> A, double* __restrict__ md, unsign
 template <int R, bool FILL>
 __global__ void k_strength(BsrView<R, R> A, const double* __restrict__ md, double beta, int* __restrict__ cnt,
                            const int* __restrict__ sptr, int* __restrict__ scol) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.nrows) return;
   int c = 0;
@@ -112,6 +116,7 @@ __global__ void k_strength(BsrView<R, R> A, const double* __restrict__ md, doubl
 enum : int { ST_UND = 0, ST_ROOT = 1, ST_MEMBER = 2, ST_ISO = 3 };
 
 __global__ void k_agg_init(const int* __restrict__ sptr, int n, int* __restrict__ st) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) st[i] = (sptr[i + 1] == sptr[i]) ? ST_ISO : ST_UND;
 }
@@ -121,6 +126,7 @@ __global__ void k_agg_init(const int* __restrict__ sptr, int n, int* __restrict_
 // changes WHEN a node decides, never WHAT it decides.
 __global__ void k_lfmis(const int* __restrict__ sptr, const int* __restrict__ scol, int n, int* st,
                         int* __restrict__ last_undecided_round, int* __restrict__ rounds_out) {
+  TMG_PDL_ENTRY;
   cg::grid_group grid = cg::this_grid();
   volatile int* vst = st;
   const int stride = gridDim.x * blockDim.x;
@@ -160,6 +166,7 @@ __global__ void k_lfmis(const int* __restrict__ sptr, const int* __restrict__ sc
 // pass-1 aggregate ids: roots by rank; members by their adjacent root; -1 isolated; -2 leftover
 __global__ void k_agg_pass1(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
                             const int* __restrict__ st, const int* __restrict__ rank, int* __restrict__ agg) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int s = st[i];
@@ -173,6 +180,7 @@ __global__ void k_agg_pass1(const int* __restrict__ sptr, const int* __restrict_
 // pass 2 pointer: lowest neighbour aggregated by pass 1, or a lower-numbered leftover
 __global__ void k_agg_pass2_ptr(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
                                 const int* __restrict__ agg1, int* __restrict__ ptr) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int t = -1;
@@ -185,6 +193,7 @@ __global__ void k_agg_pass2_ptr(const int* __restrict__ sptr, const int* __restr
 }
 __global__ void k_agg_pass2_resolve(int n, const int* __restrict__ agg1, const int* __restrict__ ptr,
                                     int* __restrict__ agg) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int a = agg1[i];
@@ -196,14 +205,17 @@ __global__ void k_agg_pass2_resolve(int n, const int* __restrict__ agg1, const i
   agg[i] = a;
 }
 __global__ void k_flag_eq(const int* __restrict__ v, int n, int val, int* __restrict__ out) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = v[i] == val ? 1 : 0;
 }
 __global__ void k_assign_isolated(int n, const int* __restrict__ rank_iso, int base, int* __restrict__ agg) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] == -1) agg[i] = base + rank_iso[i];
 }
 __global__ void k_flag_nonneg(const int* __restrict__ v, int n, int* __restrict__ out) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = v[i] >= 0 ? 1 : 0;
 }
@@ -212,6 +224,7 @@ __global__ void k_flag_nonneg(const int* __restrict__ v, int n, int* __restrict_
 __global__ void k_compact_T(int n, const int* __restrict__ agg, const int* __restrict__ rowptr,
                             const double* __restrict__ Tnode, int bsnv, int* __restrict__ col,
                             double* __restrict__ val) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || agg[i] < 0) return;
   const int p = rowptr[i];
@@ -219,14 +232,17 @@ __global__ void k_compact_T(int n, const int* __restrict__ agg, const int* __res
   for (int t = 0; t < bsnv; ++t) val[(long long)p * bsnv + t] = Tnode[(long long)i * bsnv + t];
 }
 __global__ void k_fill_value_where(int* __restrict__ agg, int n, int from, int to) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] == from) agg[i] = to;
 }
 __global__ void k_pairwise(int* __restrict__ agg, int n) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) agg[i] = i / 2;
 }
 __global__ void k_histogram(const int* __restrict__ agg, int n, int* __restrict__ size) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] >= 0) atomicAdd(size + agg[i], 1);
 }
@@ -236,6 +252,7 @@ __global__ void k_histogram(const int* __restrict__ agg, int n, int* __restrict_
 __global__ void k_merge_small_seq(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
                                   int* __restrict__ agg, int* __restrict__ size, int n_agg, int min_size,
                                   int* __restrict__ remap, int* __restrict__ n_out) {
+  TMG_PDL_ENTRY;
   if (threadIdx.x || blockIdx.x) return;
   // first loop over the originally-small aggregates, ascending
   for (int a = 0; a < n_agg; ++a) {
@@ -334,6 +351,7 @@ __device__ double block_nrm2(const double* x, int m, double* sh) {
 __global__ void k_tentative_qr(const int* __restrict__ offs, const int* __restrict__ members, int bs, int nv,
                                const double* __restrict__ B, double* __restrict__ work, const long long* woff,
                                double* __restrict__ Tval, double* __restrict__ Bc, int* __restrict__ bad) {
+  TMG_PDL_ENTRY;
   __shared__ double sh[40];
   __shared__ double tau[8];
   const int a = blockIdx.x;
@@ -434,6 +452,7 @@ __global__ void k_smooth_p(BsrView<BS, BS> A, const int* __restrict__ agg, const
                            const double* __restrict__ dinv, const double* __restrict__ rho, int* __restrict__ cnt,
                            const int* __restrict__ prow, int* __restrict__ pcol, double* __restrict__ pval,
                            int* __restrict__ overflow) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.nrows) return;
   int cols[SP_MAXC];
@@ -488,6 +507,7 @@ template <int BS, int NV>
 __global__ void k_p_from_at(int nrows, const int* __restrict__ rowptr, const int* __restrict__ col,
                             double* __restrict__ val, const int* __restrict__ agg, const double* __restrict__ Tval,
                             const double* __restrict__ dinv, const double* __restrict__ rho) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nrows) return;
   const double omega = 4.0 / (3.0 * fmax(*rho, 1e-30));
@@ -513,15 +533,18 @@ __global__ void k_p_from_at(int nrows, const int* __restrict__ rowptr, const int
 // BSR transpose and SpGEMM
 // ----------------------------------------------------------------------------
 __global__ void k_row_of(const int* __restrict__ rowptr, int nrows, int* __restrict__ rowof) {
+  TMG_PDL_ENTRY;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) rowof[p] = r;
 }
 __global__ void k_iota(int* __restrict__ v, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) v[i] = (int)i;
 }
 __global__ void k_count_cols(const int* __restrict__ col, long long nnz, int* __restrict__ cnt) {
+  TMG_PDL_ENTRY;
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p < nnz) atomicAdd(cnt + col[p], 1);
 }
@@ -529,6 +552,7 @@ __global__ void k_count_cols(const int* __restrict__ col, long long nnz, int* __
 __global__ void k_transpose_fill(const int* __restrict__ perm, const int* __restrict__ rowof,
                                  const double* __restrict__ pval, int R, int C, long long nnz,
                                  int* __restrict__ tcol, double* __restrict__ tval) {
+  TMG_PDL_ENTRY;
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (q >= nnz) return;
   const int p = perm[q];
@@ -544,6 +568,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __res
                                                                  const int* __restrict__ yp, const int* __restrict__ yc,
                                                                  int nrows, int* __restrict__ cnt,
                                                                  int* __restrict__ overflow) {
+  TMG_PDL_ENTRY;
   __shared__ int set[SG_WARPS][SG_SLOTS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * SG_WARPS + w;
@@ -581,6 +606,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __res
 // aggregate that absorbs all isolated nodes, multigrid.py:457-467) ----
 __global__ void k_heavy_bound(const int* __restrict__ xp, const int* __restrict__ xc, const int* __restrict__ yp,
                               int row, unsigned long long* __restrict__ bound) {
+  TMG_PDL_ENTRY;
   unsigned long long b = 0;
   for (int p = xp[row] + threadIdx.x; p < xp[row + 1]; p += blockDim.x) b += yp[xc[p] + 1] - yp[xc[p]];
   atomicAdd(bound, b);
@@ -588,6 +614,7 @@ __global__ void k_heavy_bound(const int* __restrict__ xp, const int* __restrict_
 __global__ void k_heavy_gather(const int* __restrict__ xp, const int* __restrict__ xc, const int* __restrict__ yp,
                                const int* __restrict__ yc, int row, int* __restrict__ out,
                                unsigned long long* __restrict__ pos) {
+  TMG_PDL_ENTRY;
   for (int p = xp[row] + blockIdx.x; p < xp[row + 1]; p += gridDim.x) {
     const int k = xc[p];
     const int len = yp[k + 1] - yp[k];
@@ -603,6 +630,7 @@ template <int R1, int K1, int C2>
 __global__ void k_heavy_fill(const int* __restrict__ xp, const int* __restrict__ xc, const double* __restrict__ xv,
                              const int* __restrict__ yp, const int* __restrict__ yc, const double* __restrict__ yv,
                              int row, const int* __restrict__ cp, const int* __restrict__ cc, double* __restrict__ cv) {
+  TMG_PDL_ENTRY;
   const int base = cp[row], nout = cp[row + 1] - base;
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= nout) return;
@@ -645,6 +673,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_fill(const int* __rest
                                                                 const int* __restrict__ cp, int* __restrict__ cc,
                                                                 double* __restrict__ cv,
                                                                 const int* __restrict__ heavy) {
+  TMG_PDL_ENTRY;
   __shared__ int set[SG_WARPS][SG_SLOTS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * SG_WARPS + w;

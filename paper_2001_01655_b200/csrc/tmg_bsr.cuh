@@ -89,6 +89,7 @@ __device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lan
 template <int R, int C>
 __global__ void __launch_bounds__(TPB) k_bsr_apply(BsrView<R, C> A, const double* __restrict__ x,
                                                    double* __restrict__ y, int accumulate) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(A, lane);
   double out[R];
@@ -107,6 +108,7 @@ template <int R, int C>
 __global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const double* __restrict__ r,
                                                       double* __restrict__ bc, const double* __restrict__ dinvc,
                                                       const double* __restrict__ wp, double* __restrict__ xc) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(Pt, lane);
   double out[R];
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const do
 template <int R>
 __global__ void __launch_bounds__(TPB) k_bsr_residual(BsrView<R, R> A, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ r) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(A, lane);
   double out[R];
@@ -142,6 +145,7 @@ template <int R, bool DOT>
 __global__ void __launch_bounds__(TPB) k_bsr_jacobi(BsrView<R, R> A, const double* __restrict__ x,
                                                     const double* __restrict__ b, const double* __restrict__ dinv,
                                                     const double* __restrict__ wp, double* __restrict__ xo, Red red) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(A, lane);
   double out[R];
@@ -165,6 +169,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_jacobi(BsrView<R, R> A, const doubl
 __global__ void k_bsr_cheb_p(const double* __restrict__ r, const double* __restrict__ p,
                              const double* __restrict__ dinv, const double* __restrict__ coef, int step,
                              double* __restrict__ po, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double beta = step == 0 ? 0.0 : coef[2 * step + 1];
@@ -176,6 +181,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_cheb(BsrView<R, R> A, const double*
                                                   const double* __restrict__ pn, const double* __restrict__ coef,
                                                   int step, int x_zero, double* __restrict__ x,
                                                   double* __restrict__ ro) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(A, lane);
   const double alpha = coef[2 * step];
@@ -195,6 +201,7 @@ template <int R>
 __global__ void __launch_bounds__(TPB) k_bsr_apply_sym(BsrView<R, R> A, const double* __restrict__ v,
                                                        const double* __restrict__ ds, double* __restrict__ tmp,
                                                        double* __restrict__ y) {
+  TMG_PDL_ENTRY;
   int lane;
   const int row = bsr_row_id(A, lane);
   double out[R];
@@ -207,6 +214,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_apply_sym(BsrView<R, R> A, const do
   }
 }
 __global__ void k_vmul(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ y, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) y[i] = a[i] * b[i];
 }
@@ -214,6 +222,7 @@ __global__ void k_vmul(const double* __restrict__ a, const double* __restrict__ 
 // scalar diagonal of a square BSR
 template <int R>
 __global__ void k_bsr_diag(BsrView<R, R> A, double* __restrict__ d, unsigned* __restrict__ bad) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.nrows) return;
   double dv[R];
@@ -234,6 +243,7 @@ __global__ void k_bsr_diag(BsrView<R, R> A, double* __restrict__ d, unsigned* __
 // dense row-major copy of a square BSR (coarsest level)
 template <int R>
 __global__ void k_bsr_to_dense(BsrView<R, R> A, double* __restrict__ Ad, long long n) {
+  TMG_PDL_ENTRY;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.nrows) return;
   for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {

@@ -3,9 +3,11 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace tmg {
@@ -41,6 +43,41 @@ inline void note_launch(long long n = 1) { launch_counter().fetch_add(n, std::me
 inline unsigned grid_for(long long n, int tpb = TPB) {
   long long g = (n + tpb - 1) / tpb;
   return (unsigned)(g < 1 ? 1 : g);
+}
+
+// Programmatic dependent launch.  Every kernel of the library starts with
+// TMG_PDL_ENTRY: wait until the preceding grid in the stream has completed and
+// its writes are visible (a no-op when launched without the PDL attribute), then
+// allow the next grid to be scheduled.  launch() adds the attribute, so the
+// next kernel's launch and block rasterisation overlap this kernel's tail -- the
+// V-cycle is ~40 dependent kernels per PCG iteration, most of them short.
+// TMG_PDL=0 disables the attribute (A/B switch).
+#define TMG_PDL_ENTRY                                                  \
+  do {                                                                 \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                 \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");    \
+  } while (0)
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TMG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TMG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 // Stream-ordered device buffer (cudaMallocAsync) -- setup never forces a device sync.

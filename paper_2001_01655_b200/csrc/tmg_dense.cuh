@@ -14,6 +14,7 @@ constexpr int GJ_NB = 32;
 // In-place Gauss-Jordan of the kb x kb pivot block; writes D = A_KK^-1.
 __global__ void __launch_bounds__(1024) k_gj_pivot(const double* __restrict__ A, long long n, long long k0, int kb,
                                                    double* __restrict__ D, unsigned* __restrict__ bad) {
+  TMG_PDL_ENTRY;
   __shared__ double M[GJ_NB][GJ_NB + 1];
   const int i = threadIdx.y, j = threadIdx.x;
   const bool in = i < kb && j < kb;
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(1024) k_gj_pivot(const double* __restrict__ A,
 __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A, long long n, long long k0, int kb,
                                                    const double* __restrict__ D, double* __restrict__ RowP,
                                                    double* __restrict__ ColP) {
+  TMG_PDL_ENTRY;
   __shared__ double Ds[GJ_NB * GJ_NB];
   for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t] = D[t];
   __syncthreads();
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A,
 __global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ A, long long n, long long k0, int kb,
                                                    const double* __restrict__ D, const double* __restrict__ RowP,
                                                    const double* __restrict__ ColP) {
+  TMG_PDL_ENTRY;
   __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[i0+ii][c]
   __shared__ double Rs[GJ_NB][64 + 1];  // Rs[c][jj] = RowP[c][j0+jj]
   __shared__ double Ds[GJ_NB][GJ_NB + 1];
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ A, long 
 // y = Ainv b: one warp per row, coalesced row reads.
 __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A, long long n,
                                                    const double* __restrict__ b, double* __restrict__ y) {
+  TMG_PDL_ENTRY;
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -143,6 +147,37 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A,
   t = warp_sum(t);
   if (lane == 0) y[row] = t;
 }
+// Even n (rows 16-byte aligned): 128-bit loads, 16 row doubles in flight per lane
+// (the coarsest inverse is 52 MB on config 1; one warp per row leaves only ~17
+// warps per SM, so bytes in flight per warp decide the bandwidth).
+__global__ void __launch_bounds__(256) k_gemv_rows2(const double* __restrict__ A, long long n,
+                                                    const double* __restrict__ b, double* __restrict__ y) {
+  TMG_PDL_ENTRY;
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double2* a = reinterpret_cast<const double2*>(A + row * n);
+  const double2* bb = reinterpret_cast<const double2*>(b);
+  const long long n2 = n >> 1;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long j = lane;
+  for (; j + 7 * 32 < n2; j += 8 * 32) {
+    double2 av[8], bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = __ldg(a + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bv[u] = __ldg(bb + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += av[u].x * bv[u].x + av[u].y * bv[u].y;
+  }
+  for (int u = 0; j < n2; j += 32, ++u) {
+    const double2 av = __ldg(a + j), bv = __ldg(bb + j);
+    s[u & 7] += av.x * bv.x + av.y * bv.y;
+  }
+  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  t = warp_sum(t);
+  if (lane == 0) y[row] = t;
+}
 
 // Dense SPD inverse on the device (setup; stream-ordered, no host sync).
 struct DenseInverse {
@@ -159,9 +194,9 @@ struct DenseInverse {
     const unsigned tiles = (unsigned)((n + 63) / 64);
     for (long long k0 = 0; k0 < n; k0 += GJ_NB) {
       const int kb = (int)std::min<long long>(GJ_NB, n - k0);
-      k_gj_pivot<<<1, dim3(GJ_NB, GJ_NB), 0, s>>>(A.get(), n, k0, kb, D.get(), bad.get()); ::tmg::note_launch();
-      k_gj_panels<<<grid_for(n), 256, 0, s>>>(A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
-      k_gj_update<<<dim3(tiles, tiles), 256, 0, s>>>(A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+      launch(k_gj_pivot, 1, dim3(GJ_NB, GJ_NB), 0, s, A.get(), n, k0, kb, D.get(), bad.get()); ::tmg::note_launch();
+      launch(k_gj_panels, grid_for(n), 256, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+      launch(k_gj_update, dim3(tiles, tiles), 256, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
     }
     TMG_CUDA(cudaGetLastError());
     RowP.release();
@@ -169,7 +204,11 @@ struct DenseInverse {
     D.release();
   }
   void apply(const double* b, double* y, cudaStream_t s) const {
-    k_gemv_rows<<<grid_for(n * 32), 256, 0, s>>>(A.get(), n, b, y); ::tmg::note_launch();
+    if ((n & 1) == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0)
+      launch(k_gemv_rows2, grid_for(n * 32), 256, 0, s, A.get(), n, b, y);
+    else
+      launch(k_gemv_rows, grid_for(n * 32), 256, 0, s, A.get(), n, b, y);
+    ::tmg::note_launch();
   }
 };
 

@@ -93,17 +93,17 @@ void with_bsr(const Level& l, F&& f) {
 template <int DIM>
 void lvl_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
   if (l.lattice())
-    with_lattice<DIM>(l, [&](auto o) { k_apply<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, x, y); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_apply<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, x, y); });
   else
-    with_bsr(l, [&](auto A, auto rr) { k_bsr_apply<decltype(rr)::value, decltype(rr)::value><<<TMG_ROW_LAUNCH(l), s>>>(A, x, y, 0); });
+    with_bsr(l, [&](auto A, auto rr) { launch(k_bsr_apply<decltype(rr)::value, decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, x, y, 0); });
   note_launch();
 }
 template <int DIM>
 void lvl_residual(const Level& l, const double* x, const double* b, double* r, cudaStream_t s) {
   if (l.lattice())
-    with_lattice<DIM>(l, [&](auto o) { k_residual<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, x, b, r); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_residual<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, x, b, r); });
   else
-    with_bsr(l, [&](auto A, auto rr) { k_bsr_residual<decltype(rr)::value><<<TMG_ROW_LAUNCH(l), s>>>(A, x, b, r); });
+    with_bsr(l, [&](auto A, auto rr) { launch(k_bsr_residual<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, x, b, r); });
   note_launch();
 }
 // one Jacobi sweep cur -> dst (cur == nullptr: zero start, x = w D^-1 b)
@@ -113,19 +113,19 @@ void lvl_sweep(const Hierarchy& H, const Level& l, const double* b, const double
   const bool block = H.sm.kind == SM_BLOCK_JACOBI;
   if (cur == nullptr && !DOT) {
     if (block)
-      k_bscale_vec<DIM><<<grid_for(l.L.n), TPB, 0, s>>>(b, l.binv.get(), l.wdev.get(), dst, l.L.n);
+      launch(k_bscale_vec<DIM>, grid_for(l.L.n), TPB, 0, s, b, l.binv.get(), l.wdev.get(), dst, l.L.n);
     else
-      k_scale_vec<<<grid_for(l.ndof), TPB, 0, s>>>(b, l.dinv.get(), l.wdev.get(), dst, l.ndof);
+      launch(k_scale_vec, grid_for(l.ndof), TPB, 0, s, b, l.dinv.get(), l.wdev.get(), dst, l.ndof);
   } else if (l.lattice()) {
     with_lattice<DIM>(l, [&](auto o) {
       if (block)
-        k_bjacobi<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, cur, b, l.binv.get(), l.wdev.get(), dst);
+        launch(k_bjacobi<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, cur, b, l.binv.get(), l.wdev.get(), dst);
       else
-        k_jacobi<DIM, decltype(o), DOT><<<TMG_NODE_LAUNCH(l), s>>>(o, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
+        launch(k_jacobi<DIM, decltype(o), DOT>, TMG_NODE_LAUNCH(l), s, o, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
     });
   } else {
     with_bsr(l, [&](auto A, auto rr) {
-      k_bsr_jacobi<decltype(rr)::value, DOT><<<TMG_ROW_LAUNCH(l), s>>>(A, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
+      launch(k_bsr_jacobi<decltype(rr)::value, DOT>, TMG_ROW_LAUNCH(l), s, A, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
     });
   }
   note_launch();
@@ -135,14 +135,14 @@ void lvl_cheb_step(const Level& l, const double* rin, const double* pin, int i, 
                    double* ro, cudaStream_t s) {
   if (l.lattice()) {
     with_lattice<DIM>(l, [&](auto o) {
-      k_cheb<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, rin, pin, l.dinv.get(), l.coef.get(), i, x_zero ? 1 : 0, x,
+      launch(k_cheb<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, rin, pin, l.dinv.get(), l.coef.get(), i, x_zero ? 1 : 0, x,
                                                            po, ro);
     });
     note_launch();
   } else {
-    k_bsr_cheb_p<<<grid_for(l.ndof), TPB, 0, s>>>(rin, pin, l.dinv.get(), l.coef.get(), i, po, l.ndof);
+    launch(k_bsr_cheb_p, grid_for(l.ndof), TPB, 0, s, rin, pin, l.dinv.get(), l.coef.get(), i, po, l.ndof);
     with_bsr(l, [&](auto A, auto rr) {
-      k_bsr_cheb<decltype(rr)::value><<<TMG_ROW_LAUNCH(l), s>>>(A, rin, po, l.coef.get(), i, x_zero ? 1 : 0, x, ro);
+      launch(k_bsr_cheb<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, rin, po, l.coef.get(), i, x_zero ? 1 : 0, x, ro);
     });
     note_launch(2);
   }
@@ -150,12 +150,12 @@ void lvl_cheb_step(const Level& l, const double* rin, const double* pin, int i, 
 template <int DIM>
 void lvl_apply_sym(Level& l, const double* v, double* y, cudaStream_t s) {
   if (l.lattice()) {
-    with_lattice<DIM>(l, [&](auto o) { k_apply_sym<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, v, l.dsq.get(), y); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_apply_sym<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, v, l.dsq.get(), y); });
     note_launch();
   } else {
-    k_vmul<<<grid_for(l.ndof), TPB, 0, s>>>(v, l.dsq.get(), l.tmp.get(), l.ndof);
+    launch(k_vmul, grid_for(l.ndof), TPB, 0, s, v, l.dsq.get(), l.tmp.get(), l.ndof);
     with_bsr(l, [&](auto A, auto rr) {
-      k_bsr_apply_sym<decltype(rr)::value><<<TMG_ROW_LAUNCH(l), s>>>(A, v, l.dsq.get(), l.tmp.get(), y);
+      launch(k_bsr_apply_sym<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, v, l.dsq.get(), l.tmp.get(), y);
     });
     note_launch(2);
   }
@@ -178,29 +178,29 @@ void lanczos_setup(Hierarchy& H, Level& l, cudaStream_t s) {
   l.lmax.alloc(1, s);
   const unsigned g = grid_for(l.ndof);
   const unsigned gr = red_grid(l.ndof);
-  k_splitmix<<<g, TPB, 0, s>>>(v.get(), l.ndof, (unsigned long long)H.sm.seed);
+  launch(k_splitmix, g, TPB, 0, s, v.get(), l.ndof, (unsigned long long)H.sm.seed);
   Red rn = H.red.red();
   rn.result = nrm.get();
-  k_dot<<<gr, TPB, 0, s>>>(v.get(), v.get(), l.ndof, rn);
-  k_div_sqrt<<<g, TPB, 0, s>>>(v.get(), nrm.get(), l.ndof);
+  launch(k_dot, gr, TPB, 0, s, v.get(), v.get(), l.ndof, rn);
+  launch(k_div_sqrt, g, TPB, 0, s, v.get(), nrm.get(), l.ndof);
   note_launch(3);
   for (int j = 0; j < m; ++j) {
     lvl_apply_sym<DIM>(l, v.get(), w.get(), s);
     Red ra = H.red.red();
     ra.result = alpha.get() + j;
-    k_dot<<<gr, TPB, 0, s>>>(w.get(), v.get(), l.ndof, ra);
-    k_lz_orth<<<g, TPB, 0, s>>>(w.get(), v.get(), vp.get(), alpha.get() + j, j > 0 ? beta2.get() + j - 1 : nullptr,
+    launch(k_dot, gr, TPB, 0, s, w.get(), v.get(), l.ndof, ra);
+    launch(k_lz_orth, g, TPB, 0, s, w.get(), v.get(), vp.get(), alpha.get() + j, j > 0 ? beta2.get() + j - 1 : nullptr,
                                 l.ndof);
     Red rb = H.red.red();
     rb.result = beta2.get() + j;
-    k_dot<<<gr, TPB, 0, s>>>(w.get(), w.get(), l.ndof, rb);
+    launch(k_dot, gr, TPB, 0, s, w.get(), w.get(), l.ndof, rb);
     note_launch(3);
     if (j + 1 < m) {
-      k_lz_next<<<g, TPB, 0, s>>>(v.get(), vp.get(), w.get(), beta2.get() + j, l.ndof);
+      launch(k_lz_next, g, TPB, 0, s, v.get(), vp.get(), w.get(), beta2.get() + j, l.ndof);
       note_launch();
     }
   }
-  k_lz_finish<<<1, 1, 0, s>>>(alpha.get(), beta2.get(), m, H.sm.degree, cheb ? l.coef.get() : nullptr, l.lmax.get(),
+  launch(k_lz_finish, 1, 1, 0, s, alpha.get(), beta2.get(), m, H.sm.degree, cheb ? l.coef.get() : nullptr, l.lmax.get(),
                               H.sm.weight, H.sm.safeguard, cheb ? nullptr : l.wdev.get());
   note_launch();
   TMG_CUDA(cudaGetLastError());
@@ -221,13 +221,13 @@ void level_setup(Hierarchy& H, Level& l, bool smoother_needed, cudaStream_t s, D
   }
   if (l.lattice())
     with_lattice<DIM>(l, [&](auto o) {
-      k_diag<DIM, decltype(o)><<<TMG_NODE_LAUNCH(l), s>>>(o, l.diag.get(), l.binv.get(), bad.get());
+      launch(k_diag<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, l.diag.get(), l.binv.get(), bad.get());
     });
   else
     with_bsr(l, [&](auto A, auto rr) {
-      k_bsr_diag<decltype(rr)::value><<<TMG_ROW_LAUNCH(l), s>>>(A, l.diag.get(), bad.get());
+      launch(k_bsr_diag<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, l.diag.get(), bad.get());
     });
-  k_recip<<<grid_for(nd), TPB, 0, s>>>(l.diag.get(), l.dinv.get(), (cheb || guard) ? l.dsq.get() : nullptr, nd);
+  launch(k_recip, grid_for(nd), TPB, 0, s, l.diag.get(), l.dinv.get(), (cheb || guard) ? l.dsq.get() : nullptr, nd);
   note_launch(2);
   l.wdev.alloc(1, s);
   TMG_CUDA(cudaMemcpyAsync(l.wdev.get(), &H.sm.weight, sizeof(double), cudaMemcpyHostToDevice, s));
@@ -244,10 +244,10 @@ void coarse_setup(Hierarchy& H, cudaStream_t s) {
   H.coarse.A.alloc((size_t)c.ndof * c.ndof, s);
   H.coarse.A.zero(s);
   if (c.lattice())
-    with_lattice<DIM>(c, [&](auto o) { k_to_dense<DIM, decltype(o)><<<TMG_NODE_LAUNCH(c), s>>>(o, H.coarse.A.get()); });
+    with_lattice<DIM>(c, [&](auto o) { launch(k_to_dense<DIM, decltype(o)>, TMG_NODE_LAUNCH(c), s, o, H.coarse.A.get()); });
   else
     with_bsr(c, [&](auto A, auto rr) {
-      k_bsr_to_dense<decltype(rr)::value><<<TMG_ROW_LAUNCH(c), s>>>(A, H.coarse.A.get(), c.ndof);
+      launch(k_bsr_to_dense<decltype(rr)::value>, TMG_ROW_LAUNCH(c), s, A, H.coarse.A.get(), c.ndof);
     });
   note_launch();
   H.coarse.build(s);
@@ -327,7 +327,7 @@ void add_geometric_levels(Hierarchy& H, const std::vector<std::array<int, 3>>& p
     l->A.alloc((size_t)Slots<DIM>::NS * DIM * DIM * l->L.n, s);
     with_lattice<DIM>(f, [&](auto o) {
       const long long nt = l->L.n * Slots<DIM>::NS;
-      k_rap<DIM, decltype(o)><<<grid_for(nt), TPB, 0, s>>>(o, T, l->A.get());
+      launch(k_rap<DIM, decltype(o)>, grid_for(nt), TPB, 0, s, o, T, l->A.get());
       note_launch();
     });
     TMG_CUDA(cudaGetLastError());
@@ -390,11 +390,11 @@ void xfer_restrict(Hierarchy& H, int k, const double* r, double* xc_first, cudaS
   Level& l = *H.lv[k];
   Level& c = *H.lv[k + 1];
   if (l.xfer == XF_GEO) {
-    k_restrict<DIM><<<node_grid<DIM>(c.L), node_block<DIM>(), 0, s>>>(l.T, r, c.b.get(), c.dinv.get(), c.wdev.get(),
+    launch(k_restrict<DIM>, node_grid<DIM>(c.L), node_block<DIM>(), 0, s, l.T, r, c.b.get(), c.dinv.get(), c.wdev.get(),
                                                                        xc_first);
   } else {
     TMG_BSR_RECT_DISPATCH(l.Pt.R, l.Pt.C,
-                          k_bsr_restrict<RR, CC><<<bsr_grid(l.Pt), TPB, 0, s>>>(
+                          launch(k_bsr_restrict<RR, CC>, bsr_grid(l.Pt), TPB, 0, s, 
                               view<RR, CC>(l.Pt), r, c.b.get(), c.dinv.get(), c.wdev.get(), xc_first))
   }
   note_launch();
@@ -404,10 +404,10 @@ void xfer_prolong_add(Hierarchy& H, int k, double* x, cudaStream_t s) {
   Level& l = *H.lv[k];
   Level& c = *H.lv[k + 1];
   if (l.xfer == XF_GEO) {
-    k_prolong_add<DIM><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(l.T, c.x.get(), x);
+    launch(k_prolong_add<DIM>, node_grid<DIM>(l.L), node_block<DIM>(), 0, s, l.T, c.x.get(), x);
   } else {
     TMG_BSR_RECT_DISPATCH(l.P.R, l.P.C,
-                          k_bsr_apply<RR, CC><<<bsr_grid(l.P), TPB, 0, s>>>(view<RR, CC>(l.P), c.x.get(), x, 1))
+                          launch(k_bsr_apply<RR, CC>, bsr_grid(l.P), TPB, 0, s, view<RR, CC>(l.P), c.x.get(), x, 1))
   }
   note_launch();
 }
@@ -456,7 +456,12 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
     if (H.n_post == 0) xcur = xout;
     TMG_CUDA(cudaMemsetAsync(xcur, 0, l.ndof * sizeof(double), s));
   }
-  const bool fuse_prolong = !cheb && H.sm.kind == SM_JACOBI && H.n_post > 0 && l.xfer == XF_GEO && l.lattice();
+  static const int fuse_mode = [] {
+    const char* e = std::getenv("TMG_FUSE_PROLONG");
+    return e ? std::atoi(e) : 0;  // measured: unfused is faster on every level
+  }();
+  const bool fuse_prolong = !cheb && H.sm.kind == SM_JACOBI && H.n_post > 0 && l.xfer == XF_GEO && l.lattice() &&
+                            (fuse_mode == 2 || (fuse_mode == 1 && l.opkind == OP_FINE));
   if (!fuse_prolong) xfer_prolong_add<DIM>(H, k, xcur, s);
   if (cheb) {
     smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);
@@ -467,10 +472,10 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
       if (p == 0 && fuse_prolong) {
         with_lattice<DIM>(l, [&](auto o) {
           if (last)
-            k_prolong_jacobi<DIM, decltype(o), true><<<TMG_NODE_LAUNCH(l), s>>>(
+            launch(k_prolong_jacobi<DIM, decltype(o), true>, TMG_NODE_LAUNCH(l), s, 
                 o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, *dot);
           else
-            k_prolong_jacobi<DIM, decltype(o), false><<<TMG_NODE_LAUNCH(l), s>>>(
+            launch(k_prolong_jacobi<DIM, decltype(o), false>, TMG_NODE_LAUNCH(l), s, 
                 o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, nored);
         });
         note_launch();

@@ -34,6 +34,7 @@ inline unsigned red_grid(long long n) { return std::min<unsigned>(grid_for(n), R
 
 __global__ void __launch_bounds__(TPB) k_dot(const double* __restrict__ a, const double* __restrict__ b, long long n,
                                              Red red) {
+  TMG_PDL_ENTRY;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -49,12 +50,14 @@ __global__ void __launch_bounds__(TPB) k_dot(const double* __restrict__ a, const
 }
 __global__ void k_scale_vec(const double* __restrict__ b, const double* __restrict__ d, const double* __restrict__ wp,
                             double* __restrict__ x, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) x[i] = *wp * (d[i] * b[i]);
 }
 template <int DIM>
 __global__ void k_bscale_vec(const double* __restrict__ b, const double* __restrict__ binv, const double* __restrict__ wp,
                              double* __restrict__ x, long long nnodes) {
+  TMG_PDL_ENTRY;
   const long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (node >= nnodes) return;
   const double w = *wp;
@@ -67,6 +70,7 @@ __global__ void k_bscale_vec(const double* __restrict__ b, const double* __restr
   }
 }
 __global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv, double* __restrict__ dsq, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   dinv[i] = 1.0 / d[i];
@@ -74,6 +78,7 @@ __global__ void k_recip(const double* __restrict__ d, double* __restrict__ dinv,
 }
 // splitmix64 start vector, bit-identical to oracle.splitmix_uniform
 __global__ void k_splitmix(double* __restrict__ v, long long n, unsigned long long seed) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned long long G = 0x9E3779B97F4A7C15ULL;
@@ -84,12 +89,14 @@ __global__ void k_splitmix(double* __restrict__ v, long long n, unsigned long lo
   v[i] = (double)(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
 }
 __global__ void k_div_sqrt(double* __restrict__ v, const double* __restrict__ s2, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) v[i] = v[i] / sqrt(*s2);
 }
 // w -= a v + b vprev  (b from beta2 slot j-1 or 0)
 __global__ void k_lz_orth(double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ vp,
                           const double* __restrict__ alpha, const double* __restrict__ beta2, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double a = *alpha;
@@ -98,6 +105,7 @@ __global__ void k_lz_orth(double* __restrict__ w, const double* __restrict__ v, 
 }
 __global__ void k_lz_next(double* __restrict__ v, double* __restrict__ vp, const double* __restrict__ w,
                           const double* __restrict__ beta2, long long n) {
+  TMG_PDL_ENTRY;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   vp[i] = v[i];
@@ -109,6 +117,7 @@ __global__ void k_lz_next(double* __restrict__ v, double* __restrict__ vp, const
 __global__ void k_lz_finish(const double* __restrict__ alpha, const double* __restrict__ beta2, int steps,
                             int degree, double* __restrict__ coef, double* __restrict__ lmax_out, double w0,
                             double sg, double* __restrict__ wout) {
+  TMG_PDL_ENTRY;
   int m = steps;
   for (int j = 0; j < steps; ++j)
     if (!(sqrt(beta2[j]) > 1e-300)) { m = j + 1; break; }

@@ -221,6 +221,8 @@ struct FineOp {
   static constexpr int EX = BX + 1, EY = BY + 1, EZ = DIM == 2 ? 1 : BZ + 1;
   static constexpr int NH = HX * HY * HZ, NEL = EX * EY * EZ;
   static constexpr size_t SMEM_BYTES = sizeof(double) * (NH * DIM + NEL) + NH;
+  // resident blocks per SM the register budget is sized for (2D: 64 regs)
+  static constexpr int MINB = DIM == 2 ? 4 : 2;
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
   // ALL threads of the block (it stages the tile and synchronises); only threads
@@ -233,29 +235,51 @@ struct FineOp {
     double* es = xs + NH * DIM;
     unsigned char* ms = reinterpret_cast<unsigned char*>(es + NEL);
     const int i0 = blockIdx.x * BX - 1, j0 = blockIdx.y * BY - 1, k0 = DIM == 3 ? (int)blockIdx.z * BZ - 1 : 0;
-    const int t0 = lin_tid(), nt = lin_nthreads();
-    for (int t = t0; t < NH; t += nt) {
+    // All loads of the tile are issued before the first shared store (the loops
+    // below are unrolled over the <= PH / PE passes of the TPB threads), so a
+    // block pays one global round trip for its tile, not one per pass.
+    const int t0 = lin_tid();
+    constexpr int PH = (NH + TPB - 1) / TPB, PE = (NEL + TPB - 1) / TPB;
+    double v[PH][DIM];
+    unsigned mk[PH];
+    double ev[PE];
+#pragma unroll
+    for (int u = 0; u < PH; ++u) {
+      const int t = t0 + u * TPB;
       const int hx = t % HX, hy = (t / HX) % HY, hz = t / (HX * HY);
       const int gi = i0 + hx, gj = j0 + hy, gk = DIM == 3 ? k0 + hz : 0;
-      double v[DIM];
-      unsigned mk = 0u;
-      if (L.inside(gi, gj, gk)) {
+      mk[u] = 0u;
+      if (t < NH && L.inside(gi, gj, gk)) {
         const int m = L.id(gi, gj, gk);
-        src.load(m, gi, gj, gk, v);
-        mk = __ldg(mask + m);
+        src.load(m, gi, gj, gk, v[u]);
+        mk[u] = __ldg(mask + m);
       } else {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) v[d] = 0.0;
+        for (int d = 0; d < DIM; ++d) v[u][d] = 0.0;
       }
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) xs[t * DIM + d] = v[d];
-      ms[t] = (unsigned char)mk;
     }
-    for (int t = t0; t < NEL; t += nt) {
+#pragma unroll
+    for (int u = 0; u < PE; ++u) {
+      const int t = t0 + u * TPB;
       const int ex = t % EX, ey = (t / EX) % EY, ez = t / (EX * EY);
-      const int gi = i0 + 1 + ex - 1, gj = j0 + 1 + ey - 1, gk = DIM == 3 ? k0 + ez : 0;
-      const bool ok = gi >= 0 && gi < ne[0] && gj >= 0 && gj < ne[1] && (DIM == 2 || (gk >= 0 && gk < ne[2]));
-      es[t] = ok ? __ldg(E + elem_id(gi, gj, gk)) : 0.0;
+      const int gi = i0 + ex, gj = j0 + ey, gk = DIM == 3 ? k0 + ez : 0;
+      const bool ok = t < NEL && gi >= 0 && gi < ne[0] && gj >= 0 && gj < ne[1] &&
+                      (DIM == 2 || (gk >= 0 && gk < ne[2]));
+      ev[u] = ok ? __ldg(E + elem_id(gi, gj, gk)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PH; ++u) {
+      const int t = t0 + u * TPB;
+      if (t < NH) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) xs[t * DIM + d] = v[u][d];
+        ms[t] = (unsigned char)mk[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PE; ++u) {
+      const int t = t0 + u * TPB;
+      if (t < NEL) es[t] = ev[u];
     }
     __syncthreads();
     if (!active) return;
@@ -351,6 +375,7 @@ struct StencilOp {
   // batch before any arithmetic) so a thread has G*(DD+DIM) loads in flight --
   // coarse levels have too few threads to hide L2 latency by occupancy alone.
   static constexpr size_t SMEM_BYTES = 0;
+  static constexpr int MINB = 1;  // full register budget: batched loads in flight
   template <class Src>
   __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
                       double self[DIM]) const {
@@ -411,8 +436,9 @@ struct StencilOp {
 
 // y = A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
                                                double* __restrict__ y) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   double out[DIM], self[DIM];
   op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
@@ -422,8 +448,9 @@ __global__ void __launch_bounds__(TPB, 1) k_apply(const __grid_constant__ Op op,
 
 // y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
                                                    const double* __restrict__ ds, double* __restrict__ y) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   double out[DIM], self[DIM], d[DIM];
   op.row(active, node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
@@ -436,13 +463,14 @@ __global__ void __launch_bounds__(TPB, 1) k_apply_sym(const __grid_constant__ Op
 
 // r = b - A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ r) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   double out[DIM], self[DIM], bb[DIM];
+  load_node<DIM>(b, node, bb);  // in flight while the tile is staged
   op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
   if (!active) return;
-  load_node<DIM>(b, node, bb);
 #pragma unroll
   for (int c = 0; c < DIM; ++c) out[c] = bb[c] - out[c];
   store_node<DIM>(r, node, out);
@@ -457,13 +485,12 @@ __device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const 
                                             double* __restrict__ xo, const Red& red) {
   TMG_NODE_IDX
   double v = 0.0;
-  double out[DIM], self[DIM];
+  double out[DIM], self[DIM], bb[DIM], d[DIM];
+  load_node<DIM>(b, node, bb);  // epilogue operands in flight while the tile is staged
+  load_node<DIM>(dinv, node, d);
+  const double w = *wp;
   op.row(active, node, ci, cj, ck, src, out, self);
   if (active) {
-    const double w = *wp;
-    double bb[DIM], d[DIM];
-    load_node<DIM>(b, node, bb);
-    load_node<DIM>(dinv, node, d);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       out[c] = self[c] + w * (d[c] * (bb[c] - out[c]));
@@ -475,28 +502,31 @@ __device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const 
 }
 
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB, 1) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                 const double* __restrict__ b, const double* __restrict__ dinv,
                                                 const double* __restrict__ wp, double* __restrict__ xo, Red red) {
+  TMG_PDL_ENTRY;
   jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
 }
 
 // first post-smoothing sweep with the coarse-grid correction fused in:
 // xs = x + P e evaluated on the fly, xo = xs + w D^-1 (b - A xs)
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB, 1) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                         const double* __restrict__ e, Coarsening T,
                                                         const double* __restrict__ b, const double* __restrict__ dinv,
                                                         const double* __restrict__ wp, double* __restrict__ xo,
                                                         Red red) {
+  TMG_PDL_ENTRY;
   jacobi_body<DIM, Op, ProlongSrc<DIM>, DOT>(op, ProlongSrc<DIM>{x, e, T}, b, dinv, wp, xo, red);
 }
 
 // xo = x + w B^-1 (b - A x), B the nodal diagonal blocks (multigrid.py:90)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                  const double* __restrict__ b, const double* __restrict__ binv,
                                                  const double* __restrict__ wp, double* __restrict__ xo) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   double out[DIM], self[DIM], r[DIM];
   op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
@@ -518,11 +548,12 @@ __global__ void __launch_bounds__(TPB, 1) k_bjacobi(const __grid_constant__ Op o
 // One Chebyshev step (multigrid.py:131 recurrence, SOR solve -> D^-1):
 //   p' = D^-1 r + beta p ; x += alpha p' ; r' = r - alpha A p'
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
                                               const double* __restrict__ p, const double* __restrict__ dinv,
                                               const double* __restrict__ coef, int step, int x_zero,
                                               double* __restrict__ x, double* __restrict__ po,
                                               double* __restrict__ ro) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
   double out[DIM], pv[DIM], rr[DIM], xv[DIM];
@@ -549,6 +580,7 @@ __global__ void __launch_bounds__(TPB, 1) k_cheb(const __grid_constant__ Op op, 
 template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, 1) k_diag(const __grid_constant__ Op op, double* __restrict__ diag,
                                               double* __restrict__ binv, unsigned* __restrict__ bad) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   if (!active) return;
   double blk[DIM * DIM];
@@ -581,6 +613,7 @@ __global__ void __launch_bounds__(TPB, 1) k_diag(const __grid_constant__ Op op, 
 // dense row-major copy of a level operator (small coarsest levels only)
 template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, 1) k_to_dense(const __grid_constant__ Op op, double* __restrict__ Ad) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   if (!active) return;
   const long long n = op.L.n * DIM;
@@ -601,6 +634,7 @@ template <int DIM>
 __global__ void __launch_bounds__(TPB, 1) k_restrict(Coarsening T, const double* __restrict__ r, double* __restrict__ bc,
                                                   const double* __restrict__ dinvc, const double* __restrict__ wp,
                                                   double* __restrict__ xc) {
+  TMG_PDL_ENTRY;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   const int J = blockIdx.y * blockDim.y + threadIdx.y;
   const int K = blockIdx.z * blockDim.z + threadIdx.z;
@@ -639,6 +673,7 @@ __global__ void __launch_bounds__(TPB, 1) k_restrict(Coarsening T, const double*
 // x += P e
 template <int DIM>
 __global__ void __launch_bounds__(TPB, 1) k_prolong_add(Coarsening T, const double* __restrict__ e, double* __restrict__ x) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z * blockDim.z + threadIdx.z;
@@ -657,6 +692,7 @@ __global__ void __launch_bounds__(TPB, 1) k_prolong_add(Coarsening T, const doub
 // provider, so level 0 is never assembled.
 template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, 1) k_rap(const __grid_constant__ Op op, Coarsening T, double* __restrict__ Ac) {
+  TMG_PDL_ENTRY;
   constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= T.C.n * NS) return;

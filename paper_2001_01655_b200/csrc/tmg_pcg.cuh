@@ -28,6 +28,7 @@ struct CgState {
 __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ bb,
                           const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h,
                           int use_cond) {
+  TMG_PDL_ENTRY;
   const double tol = cfg->rtol * sqrt(*bb);
   const double r0 = sqrt(*rr);
   st->tol = tol;
@@ -41,10 +42,11 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
 
 // p' = z + beta p (own node and, on the fly, its neighbours); q = A p'; reduce p'.q
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, 1) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
+__global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
                                                const double* __restrict__ p, double* __restrict__ pn,
                                                double* __restrict__ q, const CgState* __restrict__ st,
                                                const double* __restrict__ rz_new, Red red) {
+  TMG_PDL_ENTRY;
   TMG_NODE_IDX
   const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
   double v = 0.0;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, do
                                                    const double* __restrict__ pq, Red red,
                                                    const double* __restrict__ dinv0, const double* __restrict__ wp0,
                                                    double* __restrict__ z0) {
+  TMG_PDL_ENTRY;
   const double alpha = *rz_new / *pq;
   const double w0 = z0 ? *wp0 : 0.0;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, do
 __global__ void k_cg_check(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ rz_new,
                            const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h,
                            int use_cond) {
+  TMG_PDL_ENTRY;
   st->rz = *rz_new;
   const int it = st->it + 1;
   st->it = it;
@@ -147,7 +151,7 @@ void pcg_prologue(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0, cudaS
   const unsigned gv = red_grid(n);
   auto op0 = K.template fine<DIM>();
   if (use_x0) {
-    k_residual<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s>>>(
+    launch(k_residual<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s, 
         op0, C.x.get(), C.b.get(),
                                                                                        C.r.get());
     note_launch();
@@ -156,12 +160,12 @@ void pcg_prologue(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0, cudaS
     TMG_CUDA(cudaMemcpyAsync(C.r.get(), C.b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   if (double* z0 = pcg_z0(C, H)) {
-    k_scale_vec<<<grid_for(n), TPB, 0, s>>>(C.r.get(), H->lv[0]->dinv.get(), H->lv[0]->wdev.get(), z0, n);
+    launch(k_scale_vec, grid_for(n), TPB, 0, s, C.r.get(), H->lv[0]->dinv.get(), H->lv[0]->wdev.get(), z0, n);
     note_launch();
   }
-  k_dot<<<gv, TPB, 0, s>>>(C.b.get(), C.b.get(), n, C.bb.red());
-  k_dot<<<gv, TPB, 0, s>>>(C.r.get(), C.r.get(), n, C.rr.red());
-  k_cg_init<<<1, 1, 0, s>>>(C.cfg.get(), C.st.get(), C.bb.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
+  launch(k_dot, gv, TPB, 0, s, C.b.get(), C.b.get(), n, C.bb.red());
+  launch(k_dot, gv, TPB, 0, s, C.r.get(), C.r.get(), n, C.rr.red());
+  launch(k_cg_init, 1, 1, 0, s, C.cfg.get(), C.st.get(), C.bb.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
   note_launch(3);
   TMG_CUDA(cudaGetLastError());
 }
@@ -181,15 +185,15 @@ void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGr
     z = C.z.get();
   }
   if (!dot_done) {
-    k_dot<<<gv, TPB, 0, s>>>(C.r.get(), z, n, C.rz.red());
+    launch(k_dot, gv, TPB, 0, s, C.r.get(), z, n, C.rz.red());
     note_launch();
   }
-  k_cg_pq<DIM, decltype(op0)><<<node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s>>>(
+  launch(k_cg_pq<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s, 
       op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(), C.rz.res.get(), C.pq.red());
-  k_cg_update<<<gv, TPB, 0, s>>>(C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
+  launch(k_cg_update, gv, TPB, 0, s, C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
                                  C.pq.res.get(), C.rr.red(), z0 ? H->lv[0]->dinv.get() : nullptr,
                                  z0 ? H->lv[0]->wdev.get() : nullptr, z0);
-  k_cg_check<<<1, 1, 0, s>>>(C.cfg.get(), C.st.get(), C.rz.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
+  launch(k_cg_check, 1, 1, 0, s, C.cfg.get(), C.st.get(), C.rz.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
   note_launch(3);
   TMG_CUDA(cudaGetLastError());
 }

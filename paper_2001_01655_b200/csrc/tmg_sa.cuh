@@ -32,8 +32,10 @@ struct PhaseLog {
   }
 };
 
-__global__ void k_sqrt_to(const double* __restrict__ v2, double* __restrict__ out) { *out = sqrt(*v2); }
+__global__ void k_sqrt_to(const double* __restrict__ v2, double* __restrict__ out) {
+  TMG_PDL_ENTRY; *out = sqrt(*v2); }
 __global__ void k_clamp_agg(int* __restrict__ agg, int n, int n_reg) {
+  TMG_PDL_ENTRY;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && agg[i] >= n_reg) agg[i] = n_reg - 1;
 }

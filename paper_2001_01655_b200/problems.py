@@ -111,8 +111,8 @@ def config_0():
                                   n_pre=2, n_post=2)])
 
 
-def config_1(seed=1655):
-    nx, ny = 960, 320
+def config_1(seed=1655, dims=(960, 320)):
+    nx, ny = dims
     mesh, bc = _mbb(nx, ny)
     g = gaussian_field((nx, ny), 8.0, seed)
     rho = cone_filter(threshold(g, 0.4), 1.5)
@@ -132,8 +132,8 @@ def config_1(seed=1655):
                                   max_iterations=2000)])
 
 
-def config_2(seed=2001):
-    nx, ny = 1920, 640
+def config_2(seed=2001, dims=(1920, 640)):
+    nx, ny = dims
     mesh = build_mesh((nx, ny))
     fixed = [2 * mesh.node_index(0, j) + c for j in range(ny + 1) for c in (0, 1)]
     rng = np.random.default_rng(seed)
@@ -175,8 +175,8 @@ def _cantilever3d(nx, ny, nz):
     return mesh, BoundaryConditions(np.array(fixed), f)
 
 
-def config_3(seed=3003):
-    nx, ny, nz = 96, 48, 48
+def config_3(seed=3003, dims=(96, 48, 48)):
+    nx, ny, nz = dims
     mesh, bc = _cantilever3d(nx, ny, nz)
     g = gaussian_field((nx, ny, nz), 6.0, seed)
     rho = cone_filter(threshold(g, 0.15), 1.5)
@@ -185,8 +185,8 @@ def config_3(seed=3003):
                                   lanczos_steps=10, n_pre=1, n_post=1)])
 
 
-def config_4(seed=4004):
-    nx, ny, nz = 192, 96, 96
+def config_4(seed=4004, dims=(192, 96, 96)):
+    nx, ny, nz = dims
     mesh, bc = _cantilever3d(nx, ny, nz)
     g = gaussian_field((nx, ny, nz), 10.0, seed)
     rho = cone_filter(threshold(g, 0.12), 1.5)
