@@ -13,10 +13,14 @@ from paper_2001_01655_b200 import problems as P  # noqa: E402
 import paper_2001_01655_b200 as T  # noqa: E402
 
 c, dims = int(sys.argv[1]), tuple(int(a) for a in sys.argv[2:])
-w = P.CONFIGS[c](dims=dims)
+w = P.CONFIGS[c](dims=dims) if dims else P.CONFIGS[c]()
 E = O.simp_modulus(w.rho, 3, 1, 1e-9)
 Kd = T.assemble_stiffness(w.mesh, w.bc, E)
-h = T.build_gmg(w.mesh, Kd, 999, T.SmootherConfig(kind="chebyshev", weight=1.0), 1, 1)
+if dims:
+    h = T.build_gmg(w.mesh, Kd, 999, T.SmootherConfig(kind="chebyshev", weight=1.0), 1, 1)
+else:  # the config's own first leg
+    from bench import LegRunner
+    h = LegRunner(w, w.solvers[0]).build(Kd)
 k = h.n_levels - 1
 A = h.level_matrix(k).toarray()
 b = np.random.default_rng(0).standard_normal(A.shape[0])
