@@ -123,6 +123,96 @@ __global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ A, long 
   }
 }
 
+// The same rank-kb update on the FP64 tensor pipe: DMMA m8n8k4 (mma.sync .f64).
+// 64x64 output tile per block; warp w owns a 16x32 sub-tile = 2x4 MMA tiles.
+// Fragments (PTX m8n8k4 .f64, row.col): lane l = 4g + t holds A[g][t], B[t][g]
+// and C[g][2t..2t+1] of its 8x8 tile.  Operands come from the same shared-memory
+// panels as k_gj_update; only the pivot rows/columns take the scalar path.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256) k_gj_update_mma(double* __restrict__ A, long long n, long long k0, int kb,
+                                                       const double* __restrict__ D,
+                                                       const double* __restrict__ RowP,
+                                                       const double* __restrict__ ColP) {
+  TMG_PDL_ENTRY;
+  __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[i0+ii][c]
+  __shared__ double Rs[GJ_NB][64 + 1];  // Rs[c][jj] = RowP[c][j0+jj]
+  __shared__ double Ds[GJ_NB][GJ_NB + 1];
+  const long long i0 = blockIdx.y * 64LL, j0 = blockIdx.x * 64LL;
+  for (int t = threadIdx.x; t < GJ_NB * 64; t += blockDim.x) {
+    const int c = t / 64, q = t % 64;
+    const long long gi = i0 + q, gj = j0 + q;
+    Cs[c][q] = (c < kb && gi < n) ? ColP[gi * GJ_NB + c] : 0.0;
+    Rs[c][q] = (c < kb && gj < n) ? RowP[c * n + gj] : 0.0;
+  }
+  for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t / GJ_NB][t % GJ_NB] = D[t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int kr = (kb + 3) & ~3;  // rows c >= kb of the panels are zero
+#pragma unroll 4
+  for (int c = 0; c < kr; c += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) av[a] = Cs[c + tq][r0 + a * 8 + g];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = Rs[c + tq][c0 + b * 8 + g];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b], av[a], bv[b]);
+  }
+  const bool vec = (n & 1) == 0;  // rows 16-byte aligned: RMW the two outputs of a lane as one double2
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int ii = r0 + a * 8 + g;
+    const long long gi = i0 + ii;
+    if (gi >= n) continue;
+    const bool iK = gi >= k0 && gi < k0 + kb;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int jj0 = c0 + b * 8 + 2 * tq;
+      const long long gj0 = j0 + jj0;
+      const bool plain = vec && !iK && gj0 + 1 < n && !(gj0 + 1 >= k0 && gj0 < k0 + kb);
+      if (plain) {
+        double2* dst = reinterpret_cast<double2*>(&A[gi * n + gj0]);
+        double2 v = *dst;
+        v.x -= acc[a][b][0];
+        v.y -= acc[a][b][1];
+        *dst = v;
+        continue;
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = jj0 + e;
+        const long long gj = j0 + jj;
+        if (gj >= n) continue;
+        const bool jK = gj >= k0 && gj < k0 + kb;
+        double* dst = &A[gi * n + gj];
+        if (!iK && !jK) {
+          *dst -= acc[a][b][e];
+        } else if (iK && !jK) {
+          *dst = Rs[gi - k0][jj];
+        } else if (!iK && jK) {
+          double sacc = 0.0;
+          for (int c = 0; c < kb; ++c) sacc += Cs[c][ii] * Ds[c][gj - k0];
+          *dst = -sacc;
+        } else {
+          *dst = Ds[gi - k0][gj - k0];
+        }
+      }
+    }
+  }
+}
+
 // y = Ainv b: one warp per row, coalesced row reads.
 __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A, long long n,
                                                    const double* __restrict__ b, double* __restrict__ y) {
@@ -179,6 +269,15 @@ __global__ void __launch_bounds__(256) k_gemv_rows2(const double* __restrict__ A
   if (lane == 0) y[row] = t;
 }
 
+// TMG_DENSE_MMA=0 selects the CUDA-core update (A/B switch and parity check).
+inline bool dense_mma() {
+  static const bool on = [] {
+    const char* e = std::getenv("TMG_DENSE_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Dense SPD inverse on the device (setup; stream-ordered, no host sync).
 struct DenseInverse {
   long long n = 0;
@@ -196,7 +295,9 @@ struct DenseInverse {
       const int kb = (int)std::min<long long>(GJ_NB, n - k0);
       launch(k_gj_pivot, 1, dim3(GJ_NB, GJ_NB), 0, s, A.get(), n, k0, kb, D.get(), bad.get()); ::tmg::note_launch();
       launch(k_gj_panels, grid_for(n), 256, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
-      launch(k_gj_update, dim3(tiles, tiles), 256, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+      launch(dense_mma() ? k_gj_update_mma : k_gj_update, dim3(tiles, tiles), 256, 0, s, A.get(), n, k0, kb, D.get(),
+             RowP.get(), ColP.get());
+      ::tmg::note_launch();
     }
     TMG_CUDA(cudaGetLastError());
     RowP.release();
