@@ -171,6 +171,22 @@ int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b_dev, double
                   int32_t use_x0, const tmg_solve_desc* cfg, double* residual_history_host,
                   tmg_solve_record* rec, void* stream);
 
+/* Right-preconditioned restarted GMRES / flexible GMRES (krylov.py:48-143, the
+ * reference's default SolverHarness method).  Convergence, Givens rotations,
+ * restarts, breakdown (1e-14) and the residual history follow krylov.py; the
+ * Arnoldi step orthogonalises with CGS2 on the device.
+ * residual_history_host (may be NULL) receives iterations+1 norms (capacity
+ * max_iterations+1). */
+typedef struct {
+  double rtol;
+  int32_t max_iterations;
+  int32_t restart;
+  int32_t flexible;  /* 1: fgmres_solve (stores the preconditioned basis) */
+} tmg_gmres_desc;
+int tmg_gmres_solve(tmg_operator* K, tmg_hierarchy* h, const double* b_dev, double* x_dev,
+                    int32_t use_x0, const tmg_gmres_desc* cfg, double* residual_history_host,
+                    tmg_solve_record* rec, void* stream);
+
 /* optimization.py:106 element_strain_energies: ce_e = u_e^T KE u_e (unit modulus). */
 int tmg_strain_energy(tmg_operator* K, const double* u_dev, double* ce_dev, void* stream);
 /* optimization.py:128-129: dc_e = -p (e0-emin) rho_e^(p-1) ce_e, compliance = f.u */

@@ -8,20 +8,20 @@ entry points without the built library raises ImportError.
 """
 
 from . import _lib
-from .krylov import SolveConfig, SolveRecord, cg_solve, pcg_solve
+from .krylov import SolveConfig, SolveRecord, cg_solve, fgmres_solve, gmres_solve, pcg_solve, solve
 from .material import SimpLaw
 from .mesh import (BoundaryConditions, StiffnessOperator, StructuredMesh, assemble_stiffness,
                    build_mesh, element_stiffness, rigid_body_modes)
-from .multigrid import (MgHierarchy, SmootherConfig, build_gmg, build_hybrid, build_sa_amg,
-                        gmg_level_dims)
+from .multigrid import (AdaptiveHybridController, MgHierarchy, SmootherConfig, adapt_after_solve, build_gmg,
+                        build_hybrid, build_sa_amg, gmg_level_dims)
 from .optimization import SolverHarness, compliance_and_sensitivity, element_strain_energies
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "SolveConfig", "SolveRecord", "cg_solve", "pcg_solve", "SimpLaw", "BoundaryConditions",
+    "SolveConfig", "SolveRecord", "cg_solve", "pcg_solve", "solve", "gmres_solve", "fgmres_solve", "SimpLaw", "BoundaryConditions",
     "StiffnessOperator", "StructuredMesh", "assemble_stiffness", "build_mesh", "element_stiffness",
     "rigid_body_modes", "MgHierarchy", "SmootherConfig", "build_gmg", "build_hybrid", "build_sa_amg",
-    "gmg_level_dims",
+    "gmg_level_dims", "AdaptiveHybridController", "adapt_after_solve",
     "SolverHarness", "compliance_and_sensitivity", "element_strain_energies",
 ]

@@ -24,6 +24,11 @@ class SolveDesc(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iterations", C.c_int32)]
 
 
+class GmresDesc(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("max_iterations", C.c_int32), ("restart", C.c_int32),
+                ("flexible", C.c_int32)]
+
+
 class SolveRec(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
                 ("initial_residual", C.c_double), ("final_residual", C.c_double),
@@ -77,6 +82,8 @@ _SIGS = {
     "tmg_hierarchy_time_vcycle": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _P]),
     "tmg_pcg_solve": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolveDesc), _P,
                                 C.POINTER(SolveRec), _P]),
+    "tmg_gmres_solve": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(GmresDesc), _P,
+                                  C.POINTER(SolveRec), _P]),
     "tmg_strain_energy": (C.c_int, [_P, _P, _P, _P]),
     "tmg_compliance_sensitivity": (C.c_int, [_P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
                                              _P, _D, _P]),

@@ -4,6 +4,7 @@
 
 #include "../../include/topomg_b200.h"
 #include "tmg_pcg.cuh"
+#include "tmg_gmres.cuh"
 #include "tmg_sa.cuh"
 
 using namespace tmg;
@@ -555,6 +556,28 @@ int tmg_hierarchy_time_vcycle(tmg_hierarchy* h, int32_t level, int32_t reps, dou
   };
   if (h->h->dim == 2) run(std::integral_constant<int, 2>());
   else run(std::integral_constant<int, 3>());
+  ABI_END
+}
+
+int tmg_gmres_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x, int32_t use_x0,
+                    const tmg_gmres_desc* cfg, double* hist, tmg_solve_record* rec, void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(K && cfg, "operator/config is NULL");
+  Hierarchy* H = h ? h->h.get() : nullptr;
+  if (h) TMG_REQUIRE(h->h->lv[0]->op == &K->op, "hierarchy was built for a different operator");
+  GmresResult r = K->op.dim == 2
+                      ? gmres_solve<2>(K->op, H, b, x, use_x0 != 0, cfg->rtol, cfg->max_iterations, cfg->restart,
+                                       cfg->flexible != 0, S(stream))
+                      : gmres_solve<3>(K->op, H, b, x, use_x0 != 0, cfg->rtol, cfg->max_iterations, cfg->restart,
+                                       cfg->flexible != 0, S(stream));
+  if (hist) std::copy(r.hist.begin(), r.hist.end(), hist);
+  if (rec) {
+    rec->iterations = r.iterations;
+    rec->converged = r.converged;
+    rec->initial_residual = r.hist.front();
+    rec->final_residual = r.hist.back();
+    rec->solve_ms = r.ms;
+  }
   ABI_END
 }
 

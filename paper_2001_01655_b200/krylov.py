@@ -19,7 +19,7 @@ from ._dev import as_dev, empty_dev, ptr, stream_ptr
 
 @dataclass(frozen=True)
 class SolveConfig:
-    method: str = "cg"  # cg (device); gmres/fgmres are reference names, see DESIGN.md
+    method: str = "cg"  # cg (north-star PCG) | gmres | fgmres (reference krylov.py:17)
     rtol: float = 1e-8
     max_iterations: int = 1000
     restart: int = 200
@@ -71,8 +71,42 @@ def cg_solve(A, b, x0=None, M=None, cfg=None, out=None, stream=None):
 pcg_solve = cg_solve
 
 
+def _gmres(A, b, x0, M, cfg, flexible, stream=None):
+    b = as_dev(b)
+    n = A.shape[0]
+    if b.numel() != n:
+        raise ValueError("dimension mismatch")
+    x = empty_dev(n)
+    if x0 is not None:
+        x.copy_(as_dev(x0))
+    hist = np.zeros(cfg.max_iterations + 1)
+    rec = _lib.SolveRec()
+    desc = _lib.GmresDesc(float(cfg.rtol), int(cfg.max_iterations), int(cfg.restart), 1 if flexible else 0)
+    _lib.check(_lib.load().tmg_gmres_solve(A.handle, M.handle if M is not None else None, ptr(b), ptr(x),
+                                           1 if x0 is not None else 0, C.byref(desc), hist.ctypes.data,
+                                           C.byref(rec), stream_ptr(stream)))
+    return x, SolveRecord(iterations=int(rec.iterations), solve_time=rec.solve_ms / 1e3,
+                          residual_history=list(hist[:rec.iterations + 1]), converged=bool(rec.converged))
+
+
+def gmres_solve(A, b, x0=None, M=None, cfg=None):
+    """Restarted right-preconditioned GMRES on the device (krylov.py:134)."""
+    return _gmres(A, b, x0, M, cfg or SolveConfig(method="gmres"), flexible=False)
+
+
+def fgmres_solve(A, b, x0=None, M=None, cfg=None):
+    """Flexible GMRES on the device (krylov.py:140)."""
+    return _gmres(A, b, x0, M, cfg or SolveConfig(method="fgmres"), flexible=True)
+
+
 def solve(A, b, x0=None, M=None, cfg=None):
+    """Dispatch on cfg.method (krylov.py:146): 'cg' (the north-star PCG),
+    'gmres', 'fgmres'."""
     cfg = cfg or SolveConfig()
-    if cfg.method != "cg":
-        raise ValueError("the B200 path implements method='cg' (GMRES is a later row, DESIGN.md)")
-    return cg_solve(A, b, x0, M, cfg)
+    if cfg.method == "cg":
+        return cg_solve(A, b, x0, M, cfg)
+    if cfg.method == "fgmres":
+        return fgmres_solve(A, b, x0, M, cfg)
+    if cfg.method == "gmres":
+        return gmres_solve(A, b, x0, M, cfg)
+    raise ValueError("unknown Krylov method %r" % cfg.method)

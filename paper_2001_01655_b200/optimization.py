@@ -12,17 +12,21 @@ import numpy as np
 from . import _lib, krylov
 from ._dev import as_dev, empty_dev, ptr, stream_ptr
 from .mesh import assemble_stiffness, rigid_body_modes
-from .multigrid import DEFAULT_STRENGTH_BETA, SmootherConfig, build_gmg, build_hybrid, build_sa_amg
+from .multigrid import (DEFAULT_STRENGTH_BETA, AdaptiveHybridController, SmootherConfig, adapt_after_solve,
+                        build_gmg, build_hybrid, build_sa_amg, gmg_level_dims)
 
 
 @dataclass
 class SolverHarness:
-    """Builds a multigrid preconditioner for each operator and runs PCG
-    (optimization.py:37).  strategy: 'gmg' | 'none' on this path; 'amg' and
-    'hybrid' are the next rows."""
+    """Builds a multigrid preconditioner for each operator and runs the Krylov
+    solve on the device (optimization.py:37).  strategy: 'gmg' | 'amg' |
+    'hybrid' | 'hybrid_adaptive' | 'none'; the adaptive variant demotes one
+    geometric level after a solve that needed more than 200 iterations
+    (multigrid.py:614-631).  Extensions: n_pre/n_post/max_levels/beta/isolated
+    (the reference uses the builders' defaults)."""
 
     mesh: object
-    strategy: str = "gmg"
+    strategy: str = "amg"
     coarse_max_dofs: int = 200
     n_geo: int = 2
     smoother: SmootherConfig = field(default_factory=SmootherConfig)
@@ -34,6 +38,13 @@ class SolverHarness:
     max_levels: int | None = None
     beta: float = DEFAULT_STRENGTH_BETA
     isolated: str = "merge"
+    controller: AdaptiveHybridController | None = None
+
+    def __post_init__(self):
+        if self.strategy == "hybrid_adaptive" and self.controller is None:
+            n_levels = len(gmg_level_dims(self.mesh.dims, self.mesh.dofs_per_node, self.coarse_max_dofs))
+            start = max(2, min(self.n_geo, n_levels - 1))
+            self.controller = AdaptiveHybridController(n_geo_current=start)
 
     @property
     def near_nullspace(self):
@@ -51,8 +62,9 @@ class SolverHarness:
             h = build_sa_amg(K, self.near_nullspace, self.coarse_max_dofs, self.smoother, self.n_pre,
                              self.n_post, seed=self.seed, beta=self.beta,
                              isolated=self.isolated)
-        elif self.strategy == "hybrid":
-            h = build_hybrid(self.mesh, K, self.near_nullspace, self.n_geo, self.coarse_max_dofs,
+        elif self.strategy in ("hybrid", "hybrid_adaptive"):
+            n_geo = self.n_geo if self.strategy == "hybrid" else self.controller.n_geo_current
+            h = build_hybrid(self.mesh, K, self.near_nullspace, n_geo, self.coarse_max_dofs,
                              self.smoother, self.n_pre, self.n_post, seed=self.seed, beta=self.beta,
                              isolated=self.isolated)
         else:
@@ -64,8 +76,10 @@ class SolverHarness:
         setup = 0.0
         if hierarchy is None and self.strategy != "none":
             hierarchy, setup = self.build(K)
-        x, rec = krylov.cg_solve(K, f, x0, hierarchy, self.solve_cfg)
+        x, rec = krylov.solve(K, f, x0, hierarchy, self.solve_cfg)
         rec.setup_time = setup
+        if self.strategy == "hybrid_adaptive":
+            adapt_after_solve(self.controller, rec.iterations)
         return x, rec, hierarchy
 
 

@@ -96,3 +96,23 @@ def test_workload_generators():
     assert 0.3 < w1.rho.mean() < 0.5
     w3 = problems.config_3()
     assert w3.ndof == 97 * 49 * 49 * 3 and abs(w3.bc.load_vector.sum() + 1.0) < 1e-12
+
+
+def test_adaptive_hybrid_controller_host_logic():
+    """multigrid.py:614-631: demote one geometric level after a >200-iteration
+    solve, never below min_geo."""
+    from paper_2001_01655_b200 import AdaptiveHybridController, adapt_after_solve
+    c = AdaptiveHybridController(n_geo_current=3)
+    assert adapt_after_solve(c, 150) == "keep" and c.n_geo_current == 3
+    assert adapt_after_solve(c, 201) == "rebuild" and c.n_geo_current == 2
+    assert adapt_after_solve(c, 500) == "keep" and c.n_geo_current == 2
+    with pytest.raises(ValueError):
+        AdaptiveHybridController(n_geo_current=1)
+
+
+def test_solve_config_validation_and_methods():
+    from paper_2001_01655_b200 import SolveConfig
+    assert SolveConfig().method == "cg"
+    for bad in (dict(rtol=0.0), dict(rtol=1.0), dict(restart=0)):
+        with pytest.raises(ValueError):
+            SolveConfig(**bad)
