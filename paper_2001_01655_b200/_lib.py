@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtopomg_b200.so")
+LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(_HERE, "lib", "libtopomg_b200.so")  # TMG_LIB: A/B builds
 
 TMG_EINVAL, TMG_ERANGE, TMG_ECUDA, TMG_ENODEV, TMG_ESTATE = -1, -2, -3, -4, -5
 
