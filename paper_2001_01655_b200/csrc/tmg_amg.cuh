@@ -121,11 +121,42 @@ __global__ void k_agg_init(const int* __restrict__ sptr, int n, int* __restrict_
   if (i < n) st[i] = (sptr[i + 1] == sptr[i]) ? ST_ISO : ST_UND;
 }
 
-// Rounds of the distance-2 LFMIS in one cooperative launch.  Decisions are final
-// and monotone, so reading neighbours' states while they are being written only
-// changes WHEN a node decides, never WHAT it decides.
-__global__ void k_lfmis(const int* __restrict__ sptr, const int* __restrict__ scol, int n, int* st,
-                        int* __restrict__ last_undecided_round, int* __restrict__ rounds_out) {
+// Lower-numbered distance-1 and distance-2 neighbours of every node (the set an
+// undecided node inspects each LFMIS round), materialised once so the rounds read a flat list
+// with independent loads instead of a two-level dependent walk.  Duplicates are
+// kept: the round logic only ORs states.  FILL=false counts, FILL=true writes.
+template <bool FILL>
+__global__ void k_n2(const int* __restrict__ sptr, const int* __restrict__ scol, int n, int* __restrict__ cnt,
+                     const int* __restrict__ n2ptr, int* __restrict__ n2col) {
+  TMG_PDL_ENTRY;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  const int o = FILL ? n2ptr[i] : 0;
+  for (int p = sptr[i]; p < sptr[i + 1]; ++p) {
+    const int j = scol[p];
+    if (j < i) {
+      if (FILL) n2col[o + c] = j;
+      ++c;
+    }
+    for (int q = sptr[j]; q < sptr[j + 1]; ++q) {
+      const int k = scol[q];
+      if (k >= i) break;
+      if (FILL) n2col[o + c] = k;
+      ++c;
+    }
+  }
+  if (!FILL) cnt[i] = c;
+}
+
+// Rounds of the distance-2 LFMIS in one cooperative launch, over the flat
+// lists (8 states in flight per thread per step).  A node becomes a MEMBER if a
+// lower-numbered node within distance 2 is a ROOT, a ROOT if none of them is
+// still undecided.  Decisions are final and monotone, so reading neighbours'
+// states while they are being written only changes WHEN a node decides, never
+// WHAT it decides (the result is the sequential greedy MIS of multigrid.py:380).
+__global__ void k_lfmis2(const int* __restrict__ n2ptr, const int* __restrict__ n2col, int n, int* st,
+                         int* __restrict__ last_undecided_round, int* __restrict__ rounds_out) {
   TMG_PDL_ENTRY;
   cg::grid_group grid = cg::this_grid();
   volatile int* vst = st;
@@ -134,20 +165,19 @@ __global__ void k_lfmis(const int* __restrict__ sptr, const int* __restrict__ sc
     bool pending = false;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       if (vst[i] != ST_UND) continue;
+      const int b = n2ptr[i], e = n2ptr[i + 1];
       bool root_near = false, und_near = false;
-      for (int p = sptr[i]; p < sptr[i + 1] && !root_near; ++p) {
-        const int j = scol[p];
-        if (j < i) {
-          const int s = vst[j];
-          root_near |= s == ST_ROOT;
-          und_near |= s == ST_UND;
-        }
-        for (int q = sptr[j]; q < sptr[j + 1]; ++q) {
-          const int k = scol[q];
-          if (k >= i) break;  // sorted: only lower-numbered nodes matter
-          const int s = vst[k];
-          root_near |= s == ST_ROOT;
-          und_near |= s == ST_UND;
+      for (int p = b; p < e && !root_near; p += 8) {
+        int kk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kk[u] = p + u < e ? __ldg(n2col + p + u) : -1;
+        int sv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sv[u] = kk[u] >= 0 ? vst[kk[u]] : ST_MEMBER;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          root_near |= sv[u] == ST_ROOT;
+          und_near |= sv[u] == ST_UND;
         }
       }
       if (root_near) vst[i] = ST_MEMBER;
@@ -446,60 +476,6 @@ __device__ __forceinline__ int sorted_unique_insert(int* list, int len, int v) {
   return len + 1;
 }
 constexpr int SP_MAXC = 64;  // distinct aggregates touched by one block row of A
-
-template <int BS, int NV, bool FILL>
-__global__ void k_smooth_p(BsrView<BS, BS> A, const int* __restrict__ agg, const double* __restrict__ Tval,
-                           const double* __restrict__ dinv, const double* __restrict__ rho, int* __restrict__ cnt,
-                           const int* __restrict__ prow, int* __restrict__ pcol, double* __restrict__ pval,
-                           int* __restrict__ overflow) {
-  TMG_PDL_ENTRY;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.nrows) return;
-  int cols[SP_MAXC];
-  int nc = 0;
-  nc = sorted_unique_insert(cols, nc, agg[row]);
-  for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {
-    if (nc >= SP_MAXC) { atomicOr(overflow, 1); return; }
-    nc = sorted_unique_insert(cols, nc, agg[A.col[p]]);
-  }
-  if (!FILL) { cnt[row] = nc; return; }
-  const double omega = 4.0 / (3.0 * fmax(*rho, 1e-30));
-  double dscale[BS];
-#pragma unroll
-  for (int r = 0; r < BS; ++r) dscale[r] = __dmul_rn(omega, dinv[(long long)row * BS + r]);
-  const int base = prow[row];
-  for (int q = 0; q < nc; ++q) {
-    const int J = cols[q];
-    double S[BS][NV];
-#pragma unroll
-    for (int r = 0; r < BS; ++r)
-#pragma unroll
-      for (int c = 0; c < NV; ++c) S[r][c] = 0.0;
-    for (int p = A.rowptr[row]; p < A.rowptr[row + 1]; ++p) {
-      const int j = A.col[p];
-      if (agg[j] != J) continue;
-      const double* a = A.val + (long long)p * BS * BS;
-      const double* t = Tval + (long long)j * BS * NV;
-#pragma unroll
-      for (int r = 0; r < BS; ++r)
-#pragma unroll
-        for (int b = 0; b < BS; ++b)
-#pragma unroll
-          for (int c = 0; c < NV; ++c) S[r][c] = __dadd_rn(S[r][c], __dmul_rn(a[r * BS + b], t[b * NV + c]));
-    }
-    pcol[base + q] = J;
-    double* out = pval + (long long)(base + q) * BS * NV;
-    const bool own = J == agg[row];
-    const double* tr = Tval + (long long)row * BS * NV;
-#pragma unroll
-    for (int r = 0; r < BS; ++r)
-#pragma unroll
-      for (int c = 0; c < NV; ++c) {
-        const double x = __dmul_rn(dscale[r], S[r][c]);
-        out[r * NV + c] = own ? __dsub_rn(tr[r * NV + c], x) : -x;
-      }
-  }
-}
 
 // P from AT = A*T (same sparsity: A_ii != 0 puts agg(i) in every row of AT):
 // P_iJ = [J == agg(i)] T_i - (omega D_i^-1) (AT)_iJ, in place on AT's values.

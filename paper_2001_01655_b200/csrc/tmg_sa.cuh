@@ -212,20 +212,31 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool dr
   st.alloc(n, s); flag.alloc(1, s); flag.zero(s); rounds.alloc(1, s);
   k_agg_init<<<grid_for(n), TPB, 0, s>>>(l.sptr.get(), n, st.get());
   {
+    // flat lower-numbered distance-2 lists (count, scan, fill)
+    DevBuf<int> n2cnt, n2ptr, n2col;
+    n2cnt.alloc(n + 1, s);
+    n2cnt.zero(s);
+    k_n2<false><<<grid_for(n), TPB, 0, s>>>(l.sptr.get(), l.scol.get(), n, n2cnt.get(), nullptr, nullptr);
+    rowptr_from_counts(n2cnt, n2ptr, n, s);
+    const int n2nnz = read_int(n2ptr.get() + n, s);
+    n2col.alloc(std::max(n2nnz, 1), s);
+    k_n2<true><<<grid_for(n), TPB, 0, s>>>(l.sptr.get(), l.scol.get(), n, nullptr, n2ptr.get(), n2col.get());
+    note_launch(2);
     int dev = 0, nsm = 0, per = 0;
     TMG_CUDA(cudaGetDevice(&dev));
     TMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    TMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lfmis, TPB, 0));
+    TMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lfmis2, TPB, 0));
     const int blocks = std::max(1, std::min(nsm * per, (int)grid_for(n)));
-    const int* a0 = l.sptr.get();
-    const int* a1 = l.scol.get();
+    const int* a0 = n2ptr.get();
+    const int* a1 = n2col.get();
     int* a3 = st.get();
     int* a4 = flag.get();
     int* a5 = rounds.get();
     void* args[] = {(void*)&a0, (void*)&a1, (void*)&n, (void*)&a3, (void*)&a4, (void*)&a5};
     PhaseLog lg(s);
     lg.mark("  strength graph (nnz)", snnz);
-    TMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis, blocks, TPB, args, 0, s));
+    TMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis2, blocks, TPB, args, 0, s));
+    note_launch();
     if (lg.on) lg.mark("  LFMIS (rounds)", read_int(rounds.get(), s));
   }
   DevBuf<int> isroot, rank, agg1, ptr, isoflag, isorank;
