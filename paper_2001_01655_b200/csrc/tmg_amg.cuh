@@ -540,6 +540,13 @@ __global__ void k_transpose_fill(const int* __restrict__ perm, const int* __rest
 // Symbolic SpGEMM: number of distinct column blocks in row i of X*Y.  One warp per
 // row with a shared-memory open-addressing set.
 constexpr int SG_WARPS = 4, SG_SLOTS = 1024;
+// hash-table size for a row with at most `entries` distinct outputs: a power of
+// two >= 2 entries (load factor <= 1/2), at least one warp wide, at most SG_SLOTS
+__device__ __forceinline__ int sg_table(int entries) {
+  int t = 32;
+  while (t < 2 * entries && t < SG_SLOTS) t <<= 1;
+  return t;
+}
 __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __restrict__ xp, const int* __restrict__ xc,
                                                                  const int* __restrict__ yp, const int* __restrict__ yc,
                                                                  int nrows, int* __restrict__ cnt,
@@ -549,7 +556,13 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __res
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * SG_WARPS + w;
   if (row >= nrows) return;
-  for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
+  // table size from the product count bound: rows of the fine levels produce
+  // a handful of blocks, so clearing/probing all SG_SLOTS would dominate
+  int bound = 0;
+  for (int p = xp[row] + lane; p < xp[row + 1]; p += 32) bound += yp[xc[p] + 1] - yp[xc[p]];
+  for (int o = 16; o > 0; o >>= 1) bound += __shfl_xor_sync(0xffffffffu, bound, o);
+  const int T = sg_table(bound);
+  for (int s = lane; s < T; s += 32) set[w][s] = -1;
   __syncwarp();
   int mine = 0;
   bool full = false;
@@ -557,13 +570,13 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_count(const int* __res
     const int k = xc[p];
     for (int q = yp[k] + lane; q < yp[k + 1]; q += 32) {
       const int j = yc[q];
-      unsigned h = ((unsigned)j * 2654435761u) & (SG_SLOTS - 1);
+      unsigned h = ((unsigned)j * 2654435761u) & (T - 1);
       for (int probe = 0;; ++probe) {
-        if (probe == SG_SLOTS) { full = true; break; }
+        if (probe == T) { full = true; break; }
         const int prev = atomicCAS(&set[w][h], -1, j);
         if (prev == -1) { ++mine; break; }
         if (prev == j) break;
-        h = (h + 1) & (SG_SLOTS - 1);
+        h = (h + 1) & (T - 1);
       }
       if (full) break;
     }
@@ -651,38 +664,45 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_spgemm_fill(const int* __rest
                                                                 const int* __restrict__ heavy) {
   TMG_PDL_ENTRY;
   __shared__ int set[SG_WARPS][SG_SLOTS];
+  __shared__ int keys[SG_WARPS][SG_SLOTS / 2];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * SG_WARPS + w;
   if (row >= nrows || heavy[row]) return;
-  for (int s = lane; s < SG_SLOTS; s += 32) set[w][s] = -1;
+  const int base = cp[row];
+  const int nout = cp[row + 1] - base;
+  const int T = sg_table(nout);  // >= 2 nout: the probe always finds a slot
+  for (int s = lane; s < T; s += 32) set[w][s] = -1;
   __syncwarp();
   for (int p = xp[row]; p < xp[row + 1]; ++p) {
     const int k = xc[p];
     for (int q = yp[k] + lane; q < yp[k + 1]; q += 32) {
       const int j = yc[q];
-      unsigned h = ((unsigned)j * 2654435761u) & (SG_SLOTS - 1);
-      for (int probe = 0; probe < SG_SLOTS; ++probe) {
+      unsigned h = ((unsigned)j * 2654435761u) & (T - 1);
+      for (int probe = 0; probe < T; ++probe) {
         const int prev = atomicCAS(&set[w][h], -1, j);
         if (prev == -1 || prev == j) break;
-        h = (h + 1) & (SG_SLOTS - 1);
+        h = (h + 1) & (T - 1);
       }
     }
   }
   __syncwarp();
-  const int base = cp[row];
-  // rank of every stored key = its sorted position
-  for (int s = lane; s < SG_SLOTS; s += 32) {
-    const int key = set[w][s];
-    if (key < 0) continue;
+  // compact the stored keys (ballot), then rank each among the nout keys: its
+  // sorted position is the output column slot
+  int nk = 0;
+  for (int s0 = 0; s0 < T; s0 += 32) {
+    const int key = s0 + lane < T ? set[w][s0 + lane] : -1;
+    const unsigned b = __ballot_sync(0xffffffffu, key >= 0);
+    if (key >= 0) keys[w][nk + __popc(b & ((1u << lane) - 1u))] = key;
+    nk += __popc(b);
+  }
+  __syncwarp();
+  for (int t = lane; t < nk; t += 32) {
+    const int key = keys[w][t];
     int rank = 0;
-    for (int t = 0; t < SG_SLOTS; ++t) {
-      const int o = set[w][t];
-      rank += (o >= 0 && o < key) ? 1 : 0;
-    }
+    for (int u = 0; u < nk; ++u) rank += keys[w][u] < key ? 1 : 0;
     cc[base + rank] = key;
   }
   __syncwarp();
-  const int nout = cp[row + 1] - base;
   for (int o = lane; o < nout; o += 32) {
     const int j = cc[base + o];
     double acc[R1 * C2];
