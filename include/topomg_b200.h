@@ -162,6 +162,12 @@ int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, d
                                 void* stream);
 /* Same for one V-cycle started at `level` (diagnostics: per-level cost split). */
 int tmg_hierarchy_time_vcycle(tmg_hierarchy* h, int32_t level, int32_t reps, double* ms_host, void* stream);
+/* Same for one V-cycle phase of `level` (diagnostics): the residual, the
+ * restriction to level+1, the prolongation-add from level+1, or (last level
+ * only) the coarsest solve. */
+enum { TMG_PHASE_RESIDUAL = 0, TMG_PHASE_RESTRICT = 1, TMG_PHASE_PROLONG = 2, TMG_PHASE_COARSE = 3 };
+int tmg_hierarchy_time_phase(tmg_hierarchy* h, int32_t level, int32_t phase, int32_t reps, double* ms_host,
+                             void* stream);
 
 /* Preconditioned CG (extension; krylov.py:134 is the reference's GMRES entry).
  * h may be NULL (unpreconditioned).  x_dev holds x0 on entry when use_x0 != 0

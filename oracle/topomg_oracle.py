@@ -290,7 +290,7 @@ def simp_derivative(rho, penal, e0=1.0, emin=1e-10):
 
 @dataclass(frozen=True)
 class Smoother:
-    kind: str = "weighted_jacobi"   # weighted_jacobi | block_jacobi | chebyshev
+    kind: str = "weighted_jacobi"   # weighted_jacobi | block_jacobi | chebyshev | sor_chebyshev | sor_gmres
     weight: float = 0.5
     inner_iterations: int = 2       # Chebyshev degree
     block_size: int = 2
@@ -423,8 +423,74 @@ class JacobiChebyshevSweeps:
         return x
 
 
+class SorSolve:
+    """One forward SOR (Gauss-Seidel, omega = 1) sweep as a preconditioner solve:
+    z = tril(A)^-1 v (multigrid.py:97-106)."""
+
+    def __init__(self, A):
+        self.L = sp.tril(A, format="csr")
+        if np.any(self.L.diagonal() == 0):
+            raise ValueError("zero diagonal; SOR sweep undefined")
+
+    def solve(self, v):
+        return spla.spsolve_triangular(self.L, np.asarray(v, float), lower=True)
+
+
+class SorChebyshevSweeps:
+    """Fixed-degree Chebyshev polynomial in the SOR-preconditioned operator
+    (multigrid.py:109-150): bounds [0.1, 1.1] * lambda, lambda from 10 power
+    steps on tril(A)^-1 A from numpy default_rng(seed).standard_normal(n)."""
+
+    def __init__(self, A, cfg, seed=0):
+        self.A, self.sor, self.degree = A, SorSolve(A), cfg.inner_iterations
+        v = np.random.default_rng(seed).standard_normal(A.shape[0])
+        lam = 1.0
+        for _ in range(10):
+            v /= np.linalg.norm(v)
+            w = self.sor.solve(A @ v)
+            lam = float(np.linalg.norm(w))
+            v = w
+        self.lmax_estimate = lam
+        self.bounds = (0.1 * lam, 1.1 * lam)
+
+    def apply(self, x, b, passes):
+        lo, hi = self.bounds
+        d, c = (hi + lo) / 2.0, (hi - lo) / 2.0
+        for _ in range(passes):
+            r = b - self.A @ x
+            alpha = 0.0
+            p = None
+            for i in range(self.degree):
+                z = self.sor.solve(r)
+                if i == 0:
+                    p = z.copy()
+                    alpha = 1.0 / d
+                else:
+                    beta = (c * alpha / 2.0) ** 2
+                    alpha = 1.0 / (d - beta / alpha)
+                    p = z + beta * p
+                x = x + alpha * p
+                r = r - alpha * (self.A @ p)
+        return x
+
+
+class SorGmresSweeps:
+    """inner_iterations FGMRES steps right-preconditioned by one SOR sweep, per
+    pass (multigrid.py:153-170: rtol 1e-14, max_iterations = restart = steps)."""
+
+    def __init__(self, A, cfg):
+        self.A, self.sor, self.steps = A, SorSolve(A), cfg.inner_iterations
+
+    def apply(self, x, b, passes):
+        for _ in range(passes):
+            x, _ = gmres(self.A, b, x, self.sor.solve, rtol=1e-14, max_iterations=self.steps,
+                         restart=self.steps, flexible=True)
+        return x
+
+
 SMOOTHERS = {"weighted_jacobi": JacobiSweeps, "block_jacobi": BlockJacobiSweeps,
-             "chebyshev": JacobiChebyshevSweeps}
+             "chebyshev": JacobiChebyshevSweeps, "sor_chebyshev": SorChebyshevSweeps,
+             "sor_gmres": SorGmresSweeps}
 
 
 def make_smoother(cfg, A, block_size=None):

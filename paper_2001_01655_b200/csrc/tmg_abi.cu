@@ -559,6 +559,32 @@ int tmg_hierarchy_time_vcycle(tmg_hierarchy* h, int32_t level, int32_t reps, dou
   ABI_END
 }
 
+int tmg_hierarchy_time_phase(tmg_hierarchy* h, int32_t level, int32_t phase, int32_t reps, double* ms,
+                             void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h && reps > 0, "hierarchy is NULL or reps <= 0");
+  if (level < 0 || level > h->h->last()) throw Error(TMG_ERANGE, "level out of range");
+  const bool coarse = level == h->h->last();
+  if (coarse != (phase == TMG_PHASE_COARSE) || phase < 0 || phase > TMG_PHASE_COARSE)
+    throw Error(TMG_ERANGE, "phase not defined on this level");
+  auto run = [&](auto dimtag) {
+    constexpr int DIM = decltype(dimtag)::value;
+    Hierarchy& H = *h->h;
+    Level& l = *H.lv[level];
+    *ms = time_graph(reps, S(stream), [&](cudaStream_t cs) {
+      switch (phase) {
+        case TMG_PHASE_RESIDUAL: lvl_residual<DIM>(l, l.x.get(), l.b.get(), l.r.get(), cs); break;
+        case TMG_PHASE_RESTRICT: xfer_restrict<DIM>(H, level, l.r.get(), nullptr, cs); break;
+        case TMG_PHASE_PROLONG: xfer_prolong_add<DIM>(H, level, l.x.get(), cs); break;
+        default: H.coarse.apply(l.b.get(), l.x.get(), cs); break;
+      }
+    });
+  };
+  if (h->h->dim == 2) run(std::integral_constant<int, 2>());
+  else run(std::integral_constant<int, 3>());
+  ABI_END
+}
+
 int tmg_gmres_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x, int32_t use_x0,
                     const tmg_gmres_desc* cfg, double* hist, tmg_solve_record* rec, void* stream) {
   ABI_BEGIN

@@ -145,6 +145,39 @@ def main():
     m3 = mesh.build_mesh((3, 2, 2), (1.0, 1.0, 1.0))
     u3 = rng.standard_normal(m3.total_dofs)
     g["sens3_u"], g["sens3_ce"] = u3, optimization.element_strain_energies(m3, u3)
+    # SOR smoothers (multigrid.py:97-176) and block Jacobi on SA levels; own rng so
+    # the arrays above stay unchanged
+    rs = np.random.default_rng(11)
+    m, bc, rho, E, K = cantilever((16, 8), 2)
+    bsor = rs.standard_normal(K.shape[0])
+    g["sor2d_b"] = bsor
+    for kind in ("sor_chebyshev", "sor_gmres"):
+        hs = multigrid.build_gmg(m, K, 60, multigrid.SmootherConfig(kind=kind), 1, 1)
+        g["sor2d_%s_vc" % kind] = hs.apply(bsor)
+        if kind == "sor_chebyshev":
+            g["sor2d_lmax"] = np.array([lv.smoother.lmax_estimate for lv in hs.levels[:-1]])
+        one = multigrid.smooth(multigrid.SmootherConfig(kind=kind, inner_iterations=3), K,
+                               np.zeros(K.shape[0]), bsor, passes=2)
+        g["sor2d_%s_smooth" % kind] = one
+    # FGMRES preconditioned by a sor_gmres V-cycle (reference test_krylov.py:67)
+    hs = multigrid.build_gmg(m, K, 60, multigrid.SmootherConfig(kind="sor_gmres"))
+    x, rec = krylov.fgmres_solve(K, bc.load_vector, None, hs.apply,
+                                 krylov.SolveConfig(method="fgmres", rtol=1e-8))
+    g["sor2d_fgmres_x"], g["sor2d_fgmres_hist"] = x, np.array(rec.residual_history)
+    # SA (2D voids) with SOR smoothers and with block Jacobi (3x3 blocks below level 0)
+    mm, bcc, rr, EE, KK = cantilever((12, 8), 4, void=True)
+    B = mesh.rigid_body_modes(mm, bcc.fixed_dofs)
+    bsa = rs.standard_normal(KK.shape[0])
+    g["sorsa_b"] = bsa
+    for kind in ("sor_chebyshev", "sor_gmres", "block_jacobi"):
+        ha = multigrid.build_sa_amg(KK, B, 40, multigrid.SmootherConfig(kind=kind, weight=0.6), 1, 1)
+        g["sorsa_%s_vc" % kind] = ha.apply(bsa)
+    # 3D GMG with the SOR-Chebyshev smoother
+    m3, bc3, rho3, E3, K3 = cantilever((5, 3, 3), 3)
+    h3 = multigrid.build_gmg(m3, K3, 50, multigrid.SmootherConfig(kind="sor_chebyshev"), 1, 1)
+    b3 = rs.standard_normal(K3.shape[0])
+    g["sor3d_b"], g["sor3d_vc"] = b3, h3.apply(b3)
+    g["sor3d_lmax"] = np.array([lv.smoother.lmax_estimate for lv in h3.levels[:-1]])
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, len(g), "arrays", os.path.getsize(OUT), "bytes")
 

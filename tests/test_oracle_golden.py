@@ -172,3 +172,37 @@ def test_chebyshev_extension_reduces_error():
     xs = np.linalg.solve(A, f)
     x = sm.apply(np.zeros_like(f), f, 3)
     assert (xs - x) @ A @ (xs - x) < xs @ A @ xs
+
+
+def test_sor_smoothers_gmg(golden):
+    """SOR-Chebyshev / SOR-GMRES (multigrid.py:97-176) against the reference."""
+    g, fixed, f, rho, E, K = cantilever((16, 8), 2)
+    b = golden["sor2d_b"]
+    for kind in ("sor_chebyshev", "sor_gmres"):
+        h = O.build_gmg(g, K, 60, O.Smoother(kind), 1, 1)
+        assert rel(h.apply(b), golden["sor2d_%s_vc" % kind]) <= 1e-11
+        if kind == "sor_chebyshev":
+            lm = [lv.smoother.lmax_estimate for lv in h.levels[:-1]]
+            assert rel(lm, golden["sor2d_lmax"]) <= 1e-13
+        sm = O.make_smoother(O.Smoother(kind, inner_iterations=3), K)
+        assert rel(sm.apply(np.zeros_like(b), b, 2), golden["sor2d_%s_smooth" % kind]) <= 1e-11
+    h = O.build_gmg(g, K, 60, O.Smoother("sor_gmres"))
+    x, rec = O.gmres(K, f, None, h.apply, rtol=1e-8, flexible=True)
+    assert len(rec.residual_history) == len(golden["sor2d_fgmres_hist"])
+    assert rel(x, golden["sor2d_fgmres_x"]) <= 1e-9
+
+
+def test_sor_and_block_jacobi_sa(golden):
+    g, fixed, f, rho, E, K = cantilever((12, 8), 4, void=True)
+    B = O.rigid_body_modes(g, fixed)
+    for kind in ("sor_chebyshev", "sor_gmres", "block_jacobi"):
+        h = O.build_sa_amg(K, B, 40, O.Smoother(kind, 0.6), 1, 1)
+        assert rel(h.apply(golden["sorsa_b"]), golden["sorsa_%s_vc" % kind]) <= 1e-10
+
+
+def test_sor_chebyshev_3d(golden):
+    g, fixed, f, rho, E, K = cantilever((5, 3, 3), 3)
+    h = O.build_gmg(g, K, 50, O.Smoother("sor_chebyshev"), 1, 1)
+    lm = [lv.smoother.lmax_estimate for lv in h.levels[:-1]]
+    assert rel(lm, golden["sor3d_lmax"]) <= 1e-13
+    assert rel(h.apply(golden["sor3d_b"]), golden["sor3d_vc"]) <= 1e-11

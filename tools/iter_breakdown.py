@@ -47,6 +47,12 @@ def main():
             if k < h.n_levels - 1:
                 _lib.check(L.tmg_hierarchy_time_smoother(h.handle, k, 50, C.byref(ms), None))
                 line += "   sweep %6.2f us" % (1e3 * ms.value)
+                for ph, nm in ((0, "resid"), (1, "restrict"), (2, "prolong")):
+                    _lib.check(L.tmg_hierarchy_time_phase(h.handle, k, ph, 50, C.byref(ms), None))
+                    line += "  %s %6.2f" % (nm, 1e3 * ms.value)
+            else:
+                _lib.check(L.tmg_hierarchy_time_phase(h.handle, k, 3, 50, C.byref(ms), None))
+                line += "   coarse solve %6.2f us" % (1e3 * ms.value)
             print(line, flush=True)
 
 
