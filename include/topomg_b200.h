@@ -48,7 +48,8 @@ typedef struct {
 
 /* SmootherConfig (multigrid.py:30).  kind: 0 weighted_jacobi, 1 block_jacobi,
  * 2 chebyshev (Jacobi-preconditioned Chebyshev of degree inner_iterations with a
- * lanczos_steps-step Lanczos bound; extension required by BASELINE.json). */
+ * lanczos_steps-step Lanczos bound; extension required by BASELINE.json),
+ * 3 sor_chebyshev (multigrid.py:109), 4 sor_gmres (multigrid.py:153). */
 typedef struct {
   int32_t kind;
   double weight;
@@ -57,6 +58,10 @@ typedef struct {
   uint64_t seed;
   double safeguard;  /* weighted_jacobi only: >0 caps the weight of every level at
                         safeguard/lambda_hat(D^-1 A) (Lanczos); 0 = reference behaviour */
+  const double* power_start; /* sor_chebyshev only: the power-method start vector of
+                        multigrid.py:119, numpy.random.default_rng(0).standard_normal(ndofs)
+                        of the finest level (coarser levels use its prefix); host or
+                        device pointer, copied during the build */
 } tmg_smoother_desc;
 
 /* SolveConfig (krylov.py:17) for the preconditioned CG extension. */

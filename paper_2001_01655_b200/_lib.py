@@ -17,7 +17,8 @@ class MeshDesc(C.Structure):
 
 class SmootherDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("weight", C.c_double), ("inner_iterations", C.c_int32),
-                ("lanczos_steps", C.c_int32), ("seed", C.c_uint64), ("safeguard", C.c_double)]
+                ("lanczos_steps", C.c_int32), ("seed", C.c_uint64), ("safeguard", C.c_double),
+                ("power_start", C.c_void_p)]
 
 
 class SolveDesc(C.Structure):

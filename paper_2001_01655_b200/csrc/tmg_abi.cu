@@ -253,7 +253,9 @@ int tmg_operator_diagonal(tmg_operator* K, double* d, void* stream) {
   ABI_END
 }
 
-static SmootherCfg to_cfg(const tmg_smoother_desc* d) {
+// ndof0: rows of the finest level; keep: device copy of the sor_chebyshev power
+// start vector (host or device input), alive for the build
+static SmootherCfg to_cfg(const tmg_smoother_desc* d, long long ndof0, DevBuf<double>& keep, cudaStream_t s) {
   SmootherCfg c;
   if (d) {
     c.kind = d->kind;
@@ -265,7 +267,13 @@ static SmootherCfg to_cfg(const tmg_smoother_desc* d) {
   }
   TMG_REQUIRE(c.safeguard == 0.0 || (c.kind == SM_JACOBI && c.safeguard > 0.0 && c.safeguard < 2.0),
               "safeguard applies to weighted_jacobi only and must be in (0, 2)");
-  TMG_REQUIRE(c.kind >= 0 && c.kind <= 2, "unknown smoother kind");
+  TMG_REQUIRE(c.kind >= 0 && c.kind <= SM_SOR_GMRES, "unknown smoother kind");
+  if (c.kind == SM_SOR_CHEBYSHEV) {
+    TMG_REQUIRE(d->power_start != nullptr, "sor_chebyshev needs power_start (default_rng(0).standard_normal(ndofs))");
+    keep.alloc(ndof0, s);
+    TMG_CUDA(cudaMemcpyAsync(keep.get(), d->power_start, ndof0 * sizeof(double), cudaMemcpyDefault, s));
+    c.power_start = keep.get();
+  }
   TMG_REQUIRE(c.weight > 0.0 && c.weight <= 1.0, "smoother weight must be in (0, 1]");
   TMG_REQUIRE(c.degree >= 1, "inner_iterations must be >= 1");
   return c;
@@ -276,7 +284,8 @@ int tmg_gmg_build(tmg_operator* K, int64_t coarse_max_dofs, int32_t max_levels, 
   ABI_BEGIN
   TMG_REQUIRE(K, "operator is NULL");
   TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
-  const SmootherCfg c = to_cfg(smoother);
+  DevBuf<double> ps;
+  const SmootherCfg c = to_cfg(smoother, K->op.ndof, ps, S(stream));
   auto H = std::make_unique<tmg_hierarchy>();
   H->K = K;
   if (K->op.dim == 2)
@@ -295,8 +304,9 @@ int tmg_sa_amg_build(tmg_operator* K, const double* B_host, int32_t nvec, int64_
   TMG_REQUIRE(isolated_mode == 0 || isolated_mode == 1, "isolated_mode must be 0 (merge) or 1 (drop)");
   TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
   TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
-  const SmootherCfg c = to_cfg(smoother);
   cudaStream_t s = S(stream);
+  DevBuf<double> ps;
+  const SmootherCfg c = to_cfg(smoother, K->op.ndof, ps, s);
   const long long nd = K->op.ndof;
   DevBuf<double> B, v0;
   B.alloc(nd * nvec, s);
@@ -326,8 +336,9 @@ int tmg_hybrid_build(tmg_operator* K, int32_t n_geo, const double* Bc_host, int6
   TMG_REQUIRE(n_geo >= 1, "n_geo must be >= 1 (n_geo = 0 is build_sa_amg)");
   TMG_REQUIRE(n_pre >= 0 && n_post >= 0, "n_pre/n_post must be >= 0");
   TMG_REQUIRE(nvec == 3 || nvec == 6, "near_nullspace must be (ndofs, 3) in 2D or (ndofs, 6) in 3D");
-  const SmootherCfg c = to_cfg(smoother);
   cudaStream_t s = S(stream);
+  DevBuf<double> ps;
+  const SmootherCfg c = to_cfg(smoother, K->op.ndof, ps, s);
   DevBuf<double> B, v0;
   B.alloc(coarse_ndof * nvec, s);
   v0.alloc(coarse_ndof, s);
@@ -533,8 +544,11 @@ int tmg_hierarchy_time_smoother(tmg_hierarchy* h, int32_t level, int32_t reps, d
     Level& l = *H.lv[level];
     const Red nored{nullptr, nullptr, nullptr};
     *ms = time_graph(reps, S(stream), [&](cudaStream_t cs) {
-      if (H.sm.kind == SM_CHEBYSHEV)
-        lvl_cheb_step<DIM>(l, l.r.get(), l.p.get(), 1, false, l.x.get(), l.pt.get(), l.rt.get(), cs);
+      if (sor_kind(H.sm.kind))  // the SOR triangular solve
+        sor_solve(l, l.b.get(), l.xt.get(), cs);
+      else if (H.sm.kind == SM_CHEBYSHEV)
+        lvl_cheb_step<DIM>(l, l.r.get(), l.r.get(), l.dinv.get(), l.p.get(), 1, false, l.x.get(), l.pt.get(),
+                           l.rt.get(), cs);
       else
         lvl_sweep<DIM, false>(H, l, l.b.get(), l.x.get(), l.xt.get(), nored, cs);
     });

@@ -173,7 +173,7 @@ __global__ void k_bsr_cheb_p(const double* __restrict__ r, const double* __restr
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double beta = step == 0 ? 0.0 : coef[2 * step + 1];
-  const double z = dinv[i] * r[i];
+  const double z = dinv ? dinv[i] * r[i] : r[i];  // dinv == nullptr: r holds the SOR solve z
   po[i] = beta == 0.0 ? z : z + beta * p[i];
 }
 template <int R>

@@ -19,6 +19,7 @@
 
 #include "tmg_amg.cuh"
 #include "tmg_kern.cuh"
+#include "tmg_sor.cuh"
 
 namespace tmg {
 
@@ -45,6 +46,12 @@ struct Level {
   Bsr Tm;                        // tentative prolongation (BSR)
   DevBuf<double> Tnode;          // its blocks indexed by node (zero when unaggregated)
   DevBuf<double> rho;
+  // SOR smoothers (tmg_sor.cuh): BSR form of a lattice level, diagonal-block
+  // positions, topological ticket order, ready flags + epoch/ticket counters, and
+  // work vectors (z: SOR solve; gm*: SOR-GMRES basis V, Z, w and scalars)
+  Bsr Asor;
+  DevBuf<int> sor_diag, sor_order, sor_flag, sor_ctl;
+  DevBuf<double> z, gmV, gmZ, gmw, gmg;
   bool lattice() const { return opkind != OP_BSR; }
 };
 
@@ -86,6 +93,30 @@ template <class F>
 void with_bsr(const Level& l, F&& f) {
   TMG_BSR_SQUARE_DISPATCH(l.bs, f(view<RR, RR>(l.Ab), std::integral_constant<int, RR>{}))
 }
+// lattice level operator -> BSR (its 3^d neighbour blocks)
+template <int DIM>
+void lattice_to_bsr(const Level& l, Bsr& out, cudaStream_t s) {
+  const int n = (int)l.L.n;
+  out.nrows = out.ncols = n;
+  out.R = out.C = DIM;
+  DevBuf<int> cnt;
+  cnt.alloc(n + 1, s);
+  cnt.zero(s);
+  with_lattice<DIM>(l, [&](auto o) {
+    k_lattice_bsr_count<DIM, decltype(o)><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(o, cnt.get());
+  });
+  rowptr_from_counts(cnt, out.rowptr, n, s);
+  out.nnzb = read_int(out.rowptr.get() + n, s);
+  out.col.alloc(out.nnzb, s);
+  out.val.alloc(out.nnzb * DIM * DIM, s);
+  with_lattice<DIM>(l, [&](auto o) {
+    k_lattice_bsr_fill<DIM, decltype(o)><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(
+        o, out.rowptr.get(), out.col.get(), out.val.get());
+  });
+  note_launch(2);
+  TMG_CUDA(cudaGetLastError());
+}
+
 // launch configuration of a node kernel on level l with operator `o` in scope
 #define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), decltype(o)::SMEM_BYTES
 #define TMG_ROW_LAUNCH(l) bsr_grid((l).Ab), TPB, 0
@@ -111,6 +142,13 @@ template <int DIM, bool DOT>
 void lvl_sweep(const Hierarchy& H, const Level& l, const double* b, const double* cur, double* dst, const Red& red,
                cudaStream_t s) {
   const bool block = H.sm.kind == SM_BLOCK_JACOBI;
+  if (block && !l.lattice()) {  // nodal blocks of the SA level (multigrid.py:64 with block_size = nvec)
+    with_bsr(l, [&](auto A, auto rr) {
+      launch(k_bsr_bjacobi<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, cur, b, l.binv.get(), l.wdev.get(), dst);
+    });
+    note_launch();
+    return;
+  }
   if (cur == nullptr && !DOT) {
     if (block)
       launch(k_bscale_vec<DIM>, grid_for(l.L.n), TPB, 0, s, b, l.binv.get(), l.wdev.get(), dst, l.L.n);
@@ -131,16 +169,16 @@ void lvl_sweep(const Hierarchy& H, const Level& l, const double* b, const double
   note_launch();
 }
 template <int DIM>
-void lvl_cheb_step(const Level& l, const double* rin, const double* pin, int i, bool x_zero, double* x, double* po,
-                   double* ro, cudaStream_t s) {
+void lvl_cheb_step(const Level& l, const double* rin, const double* zs, const double* dv, const double* pin, int i,
+                   bool x_zero, double* x, double* po, double* ro, cudaStream_t s) {
   if (l.lattice()) {
     with_lattice<DIM>(l, [&](auto o) {
-      launch(k_cheb<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, rin, pin, l.dinv.get(), l.coef.get(), i, x_zero ? 1 : 0, x,
+      launch(k_cheb<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, rin, zs, pin, dv, l.coef.get(), i, x_zero ? 1 : 0, x,
                                                            po, ro);
     });
     note_launch();
   } else {
-    launch(k_bsr_cheb_p, grid_for(l.ndof), TPB, 0, s, rin, pin, l.dinv.get(), l.coef.get(), i, po, l.ndof);
+    launch(k_bsr_cheb_p, grid_for(l.ndof), TPB, 0, s, zs, pin, dv, l.coef.get(), i, po, l.ndof);
     with_bsr(l, [&](auto A, auto rr) {
       launch(k_bsr_cheb<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, rin, po, l.coef.get(), i, x_zero ? 1 : 0, x, ro);
     });
@@ -158,6 +196,152 @@ void lvl_apply_sym(Level& l, const double* v, double* y, cudaStream_t s) {
       launch(k_bsr_apply_sym<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, v, l.dsq.get(), l.tmp.get(), y);
     });
     note_launch(2);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// SOR smoothers (multigrid.py:97-176): setup and the enqueue-only solve
+// ----------------------------------------------------------------------------
+inline const Bsr& sor_matrix(const Level& l) { return l.lattice() ? l.Asor : l.Ab; }
+
+inline void dot_to(const Hierarchy& H, const double* a, const double* b, long long n, double* out, cudaStream_t s) {
+  Red r = H.red.red();
+  r.result = out;
+  launch(k_dot, red_grid(n), TPB, 0, s, a, b, n, r);
+  note_launch();
+}
+
+// Ticket order of the sync-free solve: block rows sorted by level set (length of
+// the longest chain of strictly-lower blocks ending at the row), row order inside
+// a set.  Computed on the host from the block pattern, once per level.
+inline void sor_order(const Bsr& A, DevBuf<int>& order, cudaStream_t s) {
+  const int n = A.nrows;
+  std::vector<int> rp(n + 1), col(std::max<long long>(A.nnzb, 1));
+  TMG_CUDA(cudaMemcpyAsync(rp.data(), A.rowptr.get(), (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaMemcpyAsync(col.data(), A.col.get(), A.nnzb * sizeof(int), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> depth(n);
+  int maxd = 0;
+  for (int i = 0; i < n; ++i) {
+    int d = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p)
+      if (col[p] < i) d = std::max(d, depth[col[p]] + 1);
+    depth[i] = d;
+    maxd = std::max(maxd, d);
+  }
+  std::vector<int> start(maxd + 2, 0), ord(n);
+  for (int i = 0; i < n; ++i) ++start[depth[i] + 1];
+  for (int d = 0; d <= maxd; ++d) start[d + 1] += start[d];
+  for (int i = 0; i < n; ++i) ord[start[depth[i]]++] = i;
+  order.alloc(n, s);
+  TMG_CUDA(cudaMemcpyAsync(order.get(), ord.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+}
+
+template <int DIM>
+void sor_setup(Level& l, cudaStream_t s, DevBuf<unsigned>& bad) {
+  if (l.lattice()) lattice_to_bsr<DIM>(l, l.Asor, s);
+  const Bsr& A = sor_matrix(l);
+  l.sor_diag.alloc(A.nrows, s);
+  TMG_BSR_SQUARE_DISPATCH(A.R, launch(k_sor_diagpos<RR>, grid_for(A.nrows), TPB, 0, s, view<RR, RR>(A),
+                                      l.sor_diag.get(), bad.get()))
+  note_launch();
+  sor_order(A, l.sor_order, s);
+  l.sor_flag.alloc(A.nrows, s);
+  l.sor_flag.zero(s);
+  l.sor_ctl.alloc(2, s);
+  l.sor_ctl.zero(s);
+  l.z.alloc(l.ndof, s);
+}
+
+// z = tril(A)^-1 v  (multigrid.py:105 spsolve_triangular), two launches
+inline void sor_solve(const Level& l, const double* v, double* z, cudaStream_t s) {
+  const Bsr& A = sor_matrix(l);
+  launch(k_sor_prep, 1, 1, 0, s, l.sor_ctl.get());
+  const SorView S{A.rowptr.get(), A.col.get(), A.val.get(), l.sor_diag.get(), l.sor_order.get(), A.nrows,
+                  l.sor_flag.get(), l.sor_ctl.get()};
+  const unsigned grid = (unsigned)std::min<long long>(((long long)A.nrows * 32 + SOR_TPB - 1) / SOR_TPB, 148 * 8);
+  TMG_BSR_SQUARE_DISPATCH(A.R, launch(k_sor_solve<RR>, grid, SOR_TPB, 0, s, S, v, z))
+  note_launch(2);
+}
+
+// lambda of tril(A)^-1 A by 10 power steps (multigrid.py:116-128) and the
+// Chebyshev coefficients on [0.1, 1.1] * lambda
+template <int DIM>
+void sor_cheb_setup(Hierarchy& H, Level& l, cudaStream_t s) {
+  TMG_REQUIRE(H.sm.power_start != nullptr, "sor_chebyshev needs the power-method start vector");
+  const long long nd = l.ndof;
+  DevBuf<double> v, t, nrm;
+  v.alloc(nd, s); t.alloc(nd, s); nrm.alloc(1, s);
+  TMG_CUDA(cudaMemcpyAsync(v.get(), H.sm.power_start, nd * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  l.coef.alloc(2 * std::max(H.sm.degree, 1), s);
+  l.lmax.alloc(1, s);
+  for (int it = 0; it < 10; ++it) {
+    dot_to(H, v.get(), v.get(), nd, nrm.get(), s);
+    launch(k_div_sqrt, grid_for(nd), TPB, 0, s, v.get(), nrm.get(), nd);
+    note_launch();
+    lvl_apply<DIM>(l, v.get(), t.get(), s);
+    sor_solve(l, t.get(), v.get(), s);
+  }
+  dot_to(H, v.get(), v.get(), nd, nrm.get(), s);
+  launch(k_sor_cheb_coef, 1, 1, 0, s, nrm.get(), H.sm.degree, l.coef.get(), l.lmax.get());
+  note_launch();
+  TMG_CUDA(cudaGetLastError());
+}
+
+template <int DIM>
+void sor_gmres_setup(Hierarchy& H, Level& l, cudaStream_t s) {
+  const GmLayout G{H.sm.degree};
+  l.gmV.alloc((size_t)G.M * l.ndof, s);
+  l.gmZ.alloc((size_t)G.M * l.ndof, s);
+  l.gmw.alloc(l.ndof, s);
+  l.gmg.alloc(G.size(), s);
+  l.gmg.zero(s);
+}
+
+// `passes` SOR-GMRES passes on x (in place; x_zero: x holds garbage and means 0)
+template <int DIM>
+void smooth_sor_gmres(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero, int passes, cudaStream_t s) {
+  const GmLayout G{H.sm.degree};
+  const long long n = l.ndof;
+  double* g = l.gmg.get();
+  double* V = l.gmV.get();
+  double* Z = l.gmZ.get();
+  double* w = l.gmw.get();
+  const unsigned gv = grid_for(n);
+  for (int pass = 0; pass < passes; ++pass) {
+    const double* r = b;
+    if (!x_zero) {
+      lvl_residual<DIM>(l, x, b, l.r.get(), s);
+      r = l.r.get();
+    }
+    dot_to(H, b, b, n, g + G.bb(), s);
+    dot_to(H, r, r, n, g + G.rr(), s);
+    launch(k_gm_init, 1, 1, 0, s, g, G);
+    launch(k_gm_start, gv, TPB, 0, s, r, V, g, G, n);
+    note_launch(2);
+    for (int j = 0; j < G.M; ++j) {
+      double* vj = V + (size_t)j * n;
+      double* zj = Z + (size_t)j * n;
+      sor_solve(l, vj, zj, s);
+      lvl_apply<DIM>(l, zj, w, s);
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt (krylov.py:98-100)
+        dot_to(H, V + (size_t)i * n, w, n, g + G.H(i, j), s);
+        launch(k_gm_axpy, gv, TPB, 0, s, w, V + (size_t)i * n, g, G.H(i, j), n);
+        note_launch();
+      }
+      dot_to(H, w, w, n, g + G.hn2(), s);
+      launch(k_gm_rot, 1, 1, 0, s, g, G, j);
+      note_launch();
+      if (j + 1 < G.M) {
+        launch(k_gm_next, gv, TPB, 0, s, w, V + (size_t)(j + 1) * n, g, G, n);
+        note_launch();
+      }
+    }
+    launch(k_gm_solve, 1, 1, 0, s, g, G);
+    launch(k_gm_update, gv, TPB, 0, s, x, x_zero ? 1 : 0, Z, n, g, G, n);
+    note_launch(2);
+    x_zero = false;
   }
 }
 
@@ -215,9 +399,15 @@ void level_setup(Hierarchy& H, Level& l, bool smoother_needed, cudaStream_t s, D
   const bool guard = H.sm.kind == SM_JACOBI && H.sm.safeguard > 0.0;
   if (cheb || guard) l.dsq.alloc(nd, s);
   if (H.sm.kind == SM_BLOCK_JACOBI) {
-    if (!l.lattice() && smoother_needed)
-      throw Error(-1, "block_jacobi smoothing on algebraic levels is not implemented on the B200 path");
-    l.binv.alloc(nd * DIM, s);
+    if (l.lattice()) {
+      l.binv.alloc(nd * DIM, s);
+    } else if (smoother_needed) {  // nvec x nvec nodal blocks of an SA level
+      l.binv.alloc(nd * l.Ab.R, s);
+      with_bsr(l, [&](auto A, auto rr) {
+        launch(k_bsr_block_inv<decltype(rr)::value>, grid_for(l.Ab.nrows), TPB, 0, s, A, l.binv.get(), bad.get());
+      });
+      note_launch();
+    }
   }
   if (l.lattice())
     with_lattice<DIM>(l, [&](auto o) {
@@ -232,9 +422,14 @@ void level_setup(Hierarchy& H, Level& l, bool smoother_needed, cudaStream_t s, D
   l.wdev.alloc(1, s);
   TMG_CUDA(cudaMemcpyAsync(l.wdev.get(), &H.sm.weight, sizeof(double), cudaMemcpyHostToDevice, s));
   l.b.alloc(nd, s); l.x.alloc(nd, s); l.xt.alloc(nd, s); l.r.alloc(nd, s);
-  if (cheb) { l.rt.alloc(nd, s); l.p.alloc(nd, s); l.pt.alloc(nd, s); }
+  if (cheb_kind(H.sm.kind)) { l.rt.alloc(nd, s); l.p.alloc(nd, s); l.pt.alloc(nd, s); }
   if (!l.lattice()) l.tmp.alloc(nd, s);
   if ((cheb || guard) && smoother_needed) lanczos_setup<DIM>(H, l, s);
+  if (sor_kind(H.sm.kind) && smoother_needed) {
+    sor_setup<DIM>(l, s, bad);
+    if (H.sm.kind == SM_SOR_CHEBYSHEV) sor_cheb_setup<DIM>(H, l, s);
+    else sor_gmres_setup<DIM>(H, l, s);
+  }
 }
 
 template <int DIM>
@@ -258,6 +453,7 @@ inline void finalize_checks(Hierarchy& H, DevBuf<unsigned>& bad, cudaStream_t s)
   TMG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   TMG_CUDA(cudaMemcpyAsync(&cbad, H.coarse.bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   TMG_CUDA(cudaStreamSynchronize(s));
+  if ((hbad & 5u) && sor_kind(H.sm.kind)) throw Error(-1, "zero diagonal; SOR sweep undefined");
   if (hbad & 1u) throw Error(-1, "zero diagonal entry; operator not smoothable");
   if ((hbad & 2u) && H.sm.kind == SM_BLOCK_JACOBI) throw Error(-1, "singular nodal block in block Jacobi smoother");
   if (cbad) throw Error(-5, "coarsest operator is not positive definite");
@@ -377,7 +573,14 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
       double* po = pbuf[i % 2];
       if (ro == rin) ro = rbuf[(i + 1) % 2];
       if (po == pin) po = pbuf[(i + 1) % 2];
-      lvl_cheb_step<DIM>(l, rin, pin, i, x_zero && i == 0, x, po, ro, s);
+      const double* zs = rin;
+      const double* dv = l.dinv.get();
+      if (H.sm.kind == SM_SOR_CHEBYSHEV) {  // z = SOR solve of r (multigrid.py:138)
+        sor_solve(l, rin, l.z.get(), s);
+        zs = l.z.get();
+        dv = nullptr;
+      }
+      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, ro, s);
       rin = ro;
       pin = po;
     }
@@ -424,7 +627,11 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
     return false;
   }
   Level& c = *H.lv[k + 1];
-  const bool cheb = H.sm.kind == SM_CHEBYSHEV;
+  const bool cheb = cheb_kind(H.sm.kind) || H.sm.kind == SM_SOR_GMRES;  // in-place polynomial / Krylov smoothers
+  auto smooth_poly = [&](double* x, bool x_zero, int passes) {
+    if (H.sm.kind == SM_SOR_GMRES) smooth_sor_gmres<DIM>(H, l, b, x, x_zero, passes, s);
+    else smooth_cheb<DIM>(H, l, b, x, x_zero, passes, s);
+  };
   const int W = H.n_pre + H.n_post;
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? xout : l.xt.get(); };
   const Red nored{nullptr, nullptr, nullptr};
@@ -432,7 +639,7 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
   int widx = 0;
   if (cheb) {
     if (H.n_pre > 0) {
-      smooth_cheb<DIM>(H, l, b, xout, true, H.n_pre, s);
+      smooth_poly(xout, true, H.n_pre);
       xcur = xout;
     }
   } else {
@@ -464,7 +671,7 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
                             (fuse_mode == 2 || (fuse_mode == 1 && l.opkind == OP_FINE));
   if (!fuse_prolong) xfer_prolong_add<DIM>(H, k, xcur, s);
   if (cheb) {
-    smooth_cheb<DIM>(H, l, b, xcur, false, H.n_post, s);
+    smooth_poly(xcur, false, H.n_post);
   } else {
     for (int p = 0; p < H.n_post; ++p) {
       double* dst = buf(++widx);

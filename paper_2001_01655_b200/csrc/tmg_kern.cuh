@@ -13,7 +13,9 @@
 
 namespace tmg {
 
-enum SmootherKind { SM_JACOBI = 0, SM_BLOCK_JACOBI = 1, SM_CHEBYSHEV = 2 };
+enum SmootherKind { SM_JACOBI = 0, SM_BLOCK_JACOBI = 1, SM_CHEBYSHEV = 2, SM_SOR_CHEBYSHEV = 3, SM_SOR_GMRES = 4 };
+inline bool sor_kind(int k) { return k == SM_SOR_CHEBYSHEV || k == SM_SOR_GMRES; }
+inline bool cheb_kind(int k) { return k == SM_CHEBYSHEV || k == SM_SOR_CHEBYSHEV; }
 
 struct SmootherCfg {
   int kind = SM_JACOBI;
@@ -22,6 +24,7 @@ struct SmootherCfg {
   int lanczos_steps = 10;
   uint64_t seed = 0;
   double safeguard = 0.0;  // >0: Jacobi weight capped at safeguard / lambda_hat (Lanczos)
+  const double* power_start = nullptr;  // sor_chebyshev: device start vector (>= level-0 dofs)
 };
 
 // ----------------------------------------------------------------------------

@@ -170,7 +170,7 @@ struct AxpySrc {  // z + beta * p  (beta == 0 -> z; never touches p then)
   }
 };
 template <int DIM>
-struct ChebSrc {  // dinv .* r + beta * p
+struct ChebSrc {  // dinv .* r + beta * p  (dinv == nullptr: r + beta * p)
   static constexpr bool DIRECT = true;
   const double* __restrict__ r;
   const double* __restrict__ p;
@@ -179,9 +179,14 @@ struct ChebSrc {  // dinv .* r + beta * p
   __device__ void load(int node, int, int, int, double out[DIM]) const {
     double a[DIM], d[DIM];
     load_node<DIM>(r, node, a);
-    load_node<DIM>(dinv, node, d);
+    if (dinv) {
+      load_node<DIM>(dinv, node, d);
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) out[c] = d[c] * a[c];
+      for (int c = 0; c < DIM; ++c) out[c] = d[c] * a[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] = a[c];
+    }
     if (beta != 0.0) {
       double q[DIM];
       load_node<DIM>(p, node, q);
@@ -615,11 +620,12 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_bjacobi(const __grid_constant
   store_node<DIM>(xo, node, out);
 }
 
-// One Chebyshev step (multigrid.py:131 recurrence, SOR solve -> D^-1):
-//   p' = D^-1 r + beta p ; x += alpha p' ; r' = r - alpha A p'
+// One Chebyshev step (multigrid.py:131 recurrence):
+//   p' = z + beta p ; x += alpha p' ; r' = r - alpha A p'
+// with z = D^-1 r (zs = r, Jacobi-Chebyshev) or z = SOR solve of r (zs = z, dinv = nullptr).
 template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
-                                              const double* __restrict__ p, const double* __restrict__ dinv,
+                                              const double* __restrict__ zs, const double* __restrict__ p, const double* __restrict__ dinv,
                                               const double* __restrict__ coef, int step, int x_zero,
                                               double* __restrict__ x, double* __restrict__ po,
                                               double* __restrict__ ro) {
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
   TMG_NODE_IDX
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
   double out[DIM], pv[DIM], rr[DIM], xv[DIM];
-  op.row(active, node, ci, cj, ck, ChebSrc<DIM>{r, p, dinv, beta}, out, pv);
+  op.row(active, node, ci, cj, ck, ChebSrc<DIM>{zs, p, dinv, beta}, out, pv);
   if (!active) return;
   load_node<DIM>(r, node, rr);
   if (x_zero) {

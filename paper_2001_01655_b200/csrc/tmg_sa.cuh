@@ -40,30 +40,6 @@ __global__ void k_clamp_agg(int* __restrict__ agg, int n, int n_reg) {
   if (i < n && agg[i] >= n_reg) agg[i] = n_reg - 1;
 }
 
-// lattice level operator -> BSR (its 3^d neighbour blocks)
-template <int DIM>
-void lattice_to_bsr(const Level& l, Bsr& out, cudaStream_t s) {
-  const int n = (int)l.L.n;
-  out.nrows = out.ncols = n;
-  out.R = out.C = DIM;
-  DevBuf<int> cnt;
-  cnt.alloc(n + 1, s);
-  cnt.zero(s);
-  with_lattice<DIM>(l, [&](auto o) {
-    k_lattice_bsr_count<DIM, decltype(o)><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(o, cnt.get());
-  });
-  rowptr_from_counts(cnt, out.rowptr, n, s);
-  out.nnzb = read_int(out.rowptr.get() + n, s);
-  out.col.alloc(out.nnzb, s);
-  out.val.alloc(out.nnzb * DIM * DIM, s);
-  with_lattice<DIM>(l, [&](auto o) {
-    k_lattice_bsr_fill<DIM, decltype(o)><<<node_grid<DIM>(l.L), node_block<DIM>(), 0, s>>>(
-        o, out.rowptr.get(), out.col.get(), out.val.get());
-  });
-  note_launch(2);
-  TMG_CUDA(cudaGetLastError());
-}
-
 inline void bsr_transpose(const Bsr& P, Bsr& Pt, cudaStream_t s) {
   const long long nnz = P.nnzb;
   Pt.nrows = P.ncols;

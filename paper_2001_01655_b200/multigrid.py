@@ -17,15 +17,17 @@ import numpy as np
 from . import _lib
 from ._dev import as_dev, empty_dev, ptr, stream_ptr
 
-SMOOTHER_KINDS = {"weighted_jacobi": 0, "block_jacobi": 1, "chebyshev": 2}
+SMOOTHER_KINDS = {"weighted_jacobi": 0, "block_jacobi": 1, "chebyshev": 2, "sor_chebyshev": 3, "sor_gmres": 4}
 PROVENANCE = {0: "geometric", 1: "algebraic"}
 DEFAULT_STRENGTH_BETA = 0.003  # multigrid.py:22
 
 
 @dataclass(frozen=True)
 class SmootherConfig:
-    """multigrid.py:30; kind 'chebyshev' is the Jacobi-preconditioned Chebyshev
-    extension (degree = inner_iterations, Lanczos bound over lanczos_steps)."""
+    """multigrid.py:30; kinds weighted_jacobi | block_jacobi | sor_chebyshev |
+    sor_gmres as the reference, plus 'chebyshev': the Jacobi-preconditioned
+    Chebyshev extension (degree = inner_iterations, Lanczos bound over
+    lanczos_steps)."""
 
     kind: str = "weighted_jacobi"
     weight: float = 0.5
@@ -47,10 +49,16 @@ class SmootherConfig:
     def stationary(self):
         return self.kind in ("weighted_jacobi", "block_jacobi")
 
-    def desc(self):
+    def desc(self, ndofs=0):
+        """C-ABI descriptor.  sor_chebyshev carries its power-method start vector
+        (multigrid.py:118-119: default_rng(0), the smoother is built with seed 0)
+        for the finest level's ndofs; coarser levels use its prefix."""
         if self.kind not in SMOOTHER_KINDS:
             raise ValueError("unknown smoother kind %r" % self.kind)
         d = _lib.SmootherDesc()
+        if self.kind == "sor_chebyshev":
+            d._power_start = np.ascontiguousarray(np.random.default_rng(0).standard_normal(int(ndofs)))
+            d.power_start = d._power_start.ctypes.data
         d.kind = SMOOTHER_KINDS[self.kind]
         d.weight = float(self.weight)
         d.inner_iterations = int(self.inner_iterations)
@@ -222,7 +230,7 @@ def build_gmg(mesh, K, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, max_le
         flags.append("coarse_bound_not_reached")
     h = C.c_void_p()
     _lib.check(_lib.load().tmg_gmg_build(K.handle, int(coarse_max_dofs), int(max_levels or 0),
-                                         C.byref(smoother.desc()), int(n_pre), int(n_post),
+                                         C.byref(smoother.desc(K.shape[0])), int(n_pre), int(n_post),
                                          stream_ptr(stream), C.byref(h)))
     return MgHierarchy(h, K, smoother, n_pre, n_post, flags)
 
@@ -259,7 +267,7 @@ def build_sa_amg(K, near_nullspace, coarse_max_dofs, smoother=None, n_pre=1, n_p
     v0, pv = _host_or_device(_start_vector(K.shape[0], seed) if v0 is None else v0)
     h = C.c_void_p()
     _lib.check(_lib.load().tmg_sa_amg_build(K.handle, pB, B.shape[1], int(coarse_max_dofs),
-                                            float(beta), pv, C.byref(smoother.desc()),
+                                            float(beta), pv, C.byref(smoother.desc(K.shape[0])),
                                             int(n_pre), int(n_post), isolated_mode(isolated),
                                             stream_ptr(stream), C.byref(h)))
     H = MgHierarchy(h, K, smoother, n_pre, n_post)
@@ -304,7 +312,7 @@ def build_hybrid(mesh, K, near_nullspace, n_geo, coarse_max_dofs, smoother=None,
     h = C.c_void_p()
     _lib.check(_lib.load().tmg_hybrid_build(K.handle, int(n_geo), Bc.ctypes.data, Bc.shape[0], Bc.shape[1],
                                             int(coarse_max_dofs), float(beta), v0.ctypes.data,
-                                            C.byref(smoother.desc()), int(n_pre), int(n_post),
+                                            C.byref(smoother.desc(K.shape[0])), int(n_pre), int(n_post),
                                             isolated_mode(isolated), stream_ptr(stream), C.byref(h)))
     H = MgHierarchy(h, K, smoother, n_pre, n_post)
     H.flags = H.device_flags()
