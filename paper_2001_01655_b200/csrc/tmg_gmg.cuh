@@ -260,7 +260,8 @@ inline void sor_solve(const Level& l, const double* v, double* z, cudaStream_t s
   launch(k_sor_prep, 1, 1, 0, s, l.sor_ctl.get());
   const SorView S{A.rowptr.get(), A.col.get(), A.val.get(), l.sor_diag.get(), l.sor_order.get(), A.nrows,
                   l.sor_flag.get(), l.sor_ctl.get()};
-  const unsigned grid = (unsigned)std::min<long long>(((long long)A.nrows * 32 + SOR_TPB - 1) / SOR_TPB, 148 * 8);
+  // a few hundred rows per level set are ready at a time: 4 warps per SMSP suffice
+  const unsigned grid = (unsigned)std::min<long long>(((long long)A.nrows * 32 + SOR_TPB - 1) / SOR_TPB, 148 * 2);
   TMG_BSR_SQUARE_DISPATCH(A.R, launch(k_sor_solve<RR>, grid, SOR_TPB, 0, s, S, v, z))
   note_launch(2);
 }

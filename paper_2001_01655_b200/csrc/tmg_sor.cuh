@@ -64,7 +64,13 @@ __global__ void __launch_bounds__(SOR_TPB) k_sor_solve(SorView S, const double* 
     for (int a = 0; a < R; ++a) acc[a] = 0.0;
     for (int p = beg + lane; p < dp; p += 32) {
       const int j = S.col[p];
-      while (ld_acquire(S.flag + j) != epoch) {
+      if (ld_acquire(S.flag + j) != epoch) {
+        // back off: thousands of spinning warps would otherwise saturate L2 with polls
+        unsigned ns = 32;
+        do {
+          __nanosleep(ns);
+          ns = ns < 256 ? 2 * ns : ns;
+        } while (ld_acquire(S.flag + j) != epoch);
       }
       double zj[R];
 #pragma unroll
