@@ -224,11 +224,11 @@ int tmg_operator_apply(tmg_operator* K, const double* x, double* y, void* stream
   const Operator& o = K->op;
   if (o.dim == 2) {
     auto f = o.fine<2>();
-    k_apply<2, FineOp<2>><<<node_grid<2>(o.L), node_block<2>(), FineOp<2>::SMEM_BYTES, S(stream)>>>(f, x, y);
+    launch(k_apply<2, FineOp<2>>, row_grid<2, FineOp<2>>(o.L), row_block<2, FineOp<2>>(), row_smem<FineOp<2>>(), S(stream), f, x, y);
     ::tmg::note_launch();
   } else {
     auto f = o.fine<3>();
-    k_apply<3, FineOp<3>><<<node_grid<3>(o.L), node_block<3>(), FineOp<3>::SMEM_BYTES, S(stream)>>>(f, x, y);
+    launch(k_apply<3, FineOp<3>>, row_grid<3, FineOp<3>>(o.L), row_block<3, FineOp<3>>(), row_smem<FineOp<3>>(), S(stream), f, x, y);
     ::tmg::note_launch();
   }
   TMG_CUDA(cudaGetLastError());

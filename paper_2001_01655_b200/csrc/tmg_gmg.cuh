@@ -119,12 +119,15 @@ void lattice_to_bsr(const Level& l, Bsr& out, cudaStream_t s) {
 
 // launch configuration of a node kernel on level l with operator `o` in scope
 #define TMG_NODE_LAUNCH(l) node_grid<DIM>((l).L), node_block<DIM>(), decltype(o)::SMEM_BYTES
+// row kernels (k_apply, k_residual, k_jacobi, k_bjacobi, k_cheb, k_apply_sym, k_cg_pq):
+// geometry of the operator's row path (row_grid / row_block / row_smem)
+#define TMG_ROW_OP_LAUNCH(l) TMG_ROW_OP_LAUNCH_L((l).L, o)
 #define TMG_ROW_LAUNCH(l) bsr_grid((l).Ab), TPB, 0
 
 template <int DIM>
 void lvl_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
   if (l.lattice())
-    with_lattice<DIM>(l, [&](auto o) { launch(k_apply<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, x, y); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_apply<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, x, y); });
   else
     with_bsr(l, [&](auto A, auto rr) { launch(k_bsr_apply<decltype(rr)::value, decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, x, y, 0); });
   note_launch();
@@ -132,7 +135,7 @@ void lvl_apply(const Level& l, const double* x, double* y, cudaStream_t s) {
 template <int DIM>
 void lvl_residual(const Level& l, const double* x, const double* b, double* r, cudaStream_t s) {
   if (l.lattice())
-    with_lattice<DIM>(l, [&](auto o) { launch(k_residual<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, x, b, r); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_residual<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, x, b, r); });
   else
     with_bsr(l, [&](auto A, auto rr) { launch(k_bsr_residual<decltype(rr)::value>, TMG_ROW_LAUNCH(l), s, A, x, b, r); });
   note_launch();
@@ -157,9 +160,9 @@ void lvl_sweep(const Hierarchy& H, const Level& l, const double* b, const double
   } else if (l.lattice()) {
     with_lattice<DIM>(l, [&](auto o) {
       if (block)
-        launch(k_bjacobi<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, cur, b, l.binv.get(), l.wdev.get(), dst);
+        launch(k_bjacobi<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, cur, b, l.binv.get(), l.wdev.get(), dst);
       else
-        launch(k_jacobi<DIM, decltype(o), DOT>, TMG_NODE_LAUNCH(l), s, o, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
+        launch(k_jacobi<DIM, decltype(o), DOT>, TMG_ROW_OP_LAUNCH(l), s, o, cur, b, l.dinv.get(), l.wdev.get(), dst, red);
     });
   } else {
     with_bsr(l, [&](auto A, auto rr) {
@@ -173,7 +176,7 @@ void lvl_cheb_step(const Level& l, const double* rin, const double* zs, const do
                    bool x_zero, double* x, double* po, double* ro, cudaStream_t s) {
   if (l.lattice()) {
     with_lattice<DIM>(l, [&](auto o) {
-      launch(k_cheb<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, rin, zs, pin, dv, l.coef.get(), i, x_zero ? 1 : 0, x,
+      launch(k_cheb<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, rin, zs, pin, dv, l.coef.get(), i, x_zero ? 1 : 0, x,
                                                            po, ro);
     });
     note_launch();
@@ -188,7 +191,7 @@ void lvl_cheb_step(const Level& l, const double* rin, const double* zs, const do
 template <int DIM>
 void lvl_apply_sym(Level& l, const double* v, double* y, cudaStream_t s) {
   if (l.lattice()) {
-    with_lattice<DIM>(l, [&](auto o) { launch(k_apply_sym<DIM, decltype(o)>, TMG_NODE_LAUNCH(l), s, o, v, l.dsq.get(), y); });
+    with_lattice<DIM>(l, [&](auto o) { launch(k_apply_sym<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, v, l.dsq.get(), y); });
     note_launch();
   } else {
     launch(k_vmul, grid_for(l.ndof), TPB, 0, s, v, l.dsq.get(), l.tmp.get(), l.ndof);

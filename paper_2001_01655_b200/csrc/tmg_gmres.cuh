@@ -143,7 +143,7 @@ GmresResult gmres_solve(const Operator& K, Hierarchy* H, const double* b_dev, do
   TMG_CUDA(cudaEventRecord(e0, s));
 
   auto apply_K = [&](const double* in, double* out) {
-    launch(k_apply<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s, op0,
+    launch(k_apply<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), s, op0,
            in, out);
     note_launch();
   };
@@ -166,7 +166,7 @@ GmresResult gmres_solve(const Operator& K, Hierarchy* H, const double* b_dev, do
     TMG_CUDA(cudaStreamSynchronize(s));
   };
   auto residual = [&]() {  // r = b - K x
-    launch(k_residual<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s,
+    launch(k_residual<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), s,
            op0, (const double*)x_dev, b_dev, r.get());
     note_launch();
   };

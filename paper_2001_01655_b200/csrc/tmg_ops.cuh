@@ -234,7 +234,18 @@ struct FineOp {
   static constexpr int NH = HX * HY * HZ, NEL = EX * EY * EZ;
   static constexpr size_t SMEM_BYTES = sizeof(double) * (NH * DIM + NEL) + NH;
   // resident blocks per SM the register budget is sized for (2D: 64 regs)
-  static constexpr int MINB = DIM == 2 ? 4 : 2;
+#ifndef TMG_F3_MINB
+#define TMG_F3_MINB 3  // 3D: 80 registers, 3 CTAs per SM (measured best of 2/3/4)
+#endif
+  static constexpr int MINB = DIM == 2 ? 4 : TMG_F3_MINB;
+  // 3D pair rows (tmg_fine3.cuh, fine3_rows: two x-adjacent nodes per thread)
+  // are an A/B build option (-DTMG_FINE3_PAIR); measured on par with the tile
+  // (201 vs 194 us per config-4 sweep), so the tile stays the default.
+#ifdef TMG_FINE3_PAIR
+  static constexpr bool STREAM = DIM == 3;
+#else
+  static constexpr bool STREAM = false;
+#endif
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
   // ALL threads of the block (it stages the tile and synchronises); only threads
@@ -342,13 +353,22 @@ struct FineOp {
                       (DIM == 2 || (gk >= 0 && gk < ne[2]));
       ev[u] = ok ? __ldg(E + elem_id(gi, gj, gk)) : 0.0;
     }
+    // 3D: the tile holds masked values (each staged value is read by up to 27
+    // threads; masking once here removes 81 selects per row), the row's own
+    // unmasked value and mask come straight from global memory
+    constexpr bool PREMASK = DIM == 3;
+    unsigned self_mk = 0u;
+    if (PREMASK && active) {
+      src.load(node, i, j, k, self);
+      self_mk = __ldg(mask + node);
+    }
 #pragma unroll
     for (int u = 0; u < PH; ++u) {
       const int t = t0 + u * TPB;
       if (t < NH) {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) xs[t * DIM + d] = v[u][d];
-        ms[t] = (unsigned char)mk[u];
+        for (int d = 0; d < DIM; ++d) xs[t * DIM + d] = (!PREMASK || ((mk[u] >> d) & 1u)) ? v[u][d] : 0.0;
+        if (!PREMASK) ms[t] = (unsigned char)mk[u];
       }
     }
 #pragma unroll
@@ -365,12 +385,17 @@ struct FineOp {
     for (int s = 0; s < NS; ++s) {
       const int h = (tx + 1 + Slots<DIM>::dx(s)) + HX * ((ty + 1 + Slots<DIM>::dy(s)) + HY * (tz + (DIM == 3 ? 1 : 0) +
                                                                                                 Slots<DIM>::dz(s)));
-      const unsigned mk = ms[h];
+      if constexpr (PREMASK) {
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const double v = xs[h * DIM + d];
-        if (s == NS / 2) self[d] = v;
-        xv[s][d] = ((mk >> d) & 1u) ? v : 0.0;
+        for (int d = 0; d < DIM; ++d) xv[s][d] = xs[h * DIM + d];
+      } else {
+        const unsigned mk = ms[h];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          const double v = xs[h * DIM + d];
+          if (s == NS / 2) self[d] = v;
+          xv[s][d] = ((mk >> d) & 1u) ? v : 0.0;
+        }
       }
     }
     double acc[DIM];
@@ -399,7 +424,7 @@ struct FineOp {
 #pragma unroll
           for (int c = 0; c < DIM; ++c) acc[c] += Ee * t[c];
         }
-    const unsigned mn = ms[(tx + 1) + HX * ((ty + 1) + HY * (tz + (DIM == 3 ? 1 : 0)))];
+    const unsigned mn = PREMASK ? self_mk : ms[(tx + 1) + HX * ((ty + 1) + HY * (tz + (DIM == 3 ? 1 : 0)))];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) out[c] = ((mn >> c) & 1u) ? acc[c] : self[c];
   }
@@ -437,6 +462,10 @@ struct FineOp {
   }
 };
 
+}  // namespace tmg
+#include "tmg_fine3.cuh"
+namespace tmg {
+
 // ----------------------------------------------------------------------------
 // StencilOp
 // ----------------------------------------------------------------------------
@@ -451,6 +480,7 @@ struct StencilOp {
   // coarse levels have too few threads to hide L2 latency by occupancy alone.
   static constexpr size_t SMEM_BYTES = 0;
   static constexpr int MINB = 1;  // full register budget: batched loads in flight
+  static constexpr bool STREAM = false;
   template <class Src>
   __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
                       double self[DIM]) const {
@@ -499,6 +529,26 @@ struct StencilOp {
   }
 };
 
+// launch geometry of the row kernels below: streamed operators (FineOp<3>)
+// launch one CTA per 16x16 node column and z-chunk, the others one thread per node
+template <int DIM, class Op>
+inline dim3 row_grid(const Lat& L) {
+  if constexpr (Op::STREAM) return f3::grid(L);
+  else return node_grid<DIM>(L);
+}
+template <int DIM, class Op>
+inline dim3 row_block() {
+  if constexpr (Op::STREAM) return dim3(f3::NT, 1, 1);
+  else return node_block<DIM>();
+}
+template <class Op>
+constexpr size_t row_smem() {
+  if constexpr (Op::STREAM) return f3::SMEM_BYTES;
+  else return Op::SMEM_BYTES;
+}
+#define TMG_ROW_OP_LAUNCH_L(Lat_, op_) \
+  row_grid<DIM, decltype(op_)>(Lat_), row_block<DIM, decltype(op_)>(), row_smem<decltype(op_)>()
+
 // ----------------------------------------------------------------------------
 // generic node-parallel kernels (2D/3D launch: node_grid / node_block)
 // ----------------------------------------------------------------------------
@@ -514,11 +564,17 @@ template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, Op::MINB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
                                                double* __restrict__ y) {
   TMG_PDL_ENTRY;
-  TMG_NODE_IDX
-  double out[DIM], self[DIM];
-  op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
-  if (!active) return;
-  store_node<DIM>(y, node, out);
+  if constexpr (Op::STREAM) {
+    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* out, const double*) {
+      store_node<DIM>(y, node, out);
+    });
+  } else {
+    TMG_NODE_IDX
+    double out[DIM], self[DIM];
+    op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+    if (!active) return;
+    store_node<DIM>(y, node, out);
+  }
 }
 
 // y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
@@ -526,14 +582,24 @@ template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, Op::MINB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
                                                    const double* __restrict__ ds, double* __restrict__ y) {
   TMG_PDL_ENTRY;
-  TMG_NODE_IDX
-  double out[DIM], self[DIM], d[DIM];
-  op.row(active, node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
-  if (!active) return;
-  load_node<DIM>(ds, node, d);
+  if constexpr (Op::STREAM) {
+    fine3_rows(op, ScaledSrc<DIM>{v, ds}, [&](int node, int, int, int, const double* o, const double*) {
+      double d[DIM], out[DIM];
+      load_node<DIM>(ds, node, d);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) out[c] *= d[c];
-  store_node<DIM>(y, node, out);
+      for (int c = 0; c < DIM; ++c) out[c] = o[c] * d[c];
+      store_node<DIM>(y, node, out);
+    });
+  } else {
+    TMG_NODE_IDX
+    double out[DIM], self[DIM], d[DIM];
+    op.row(active, node, ci, cj, ck, ScaledSrc<DIM>{v, ds}, out, self);
+    if (!active) return;
+    load_node<DIM>(ds, node, d);
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] *= d[c];
+    store_node<DIM>(y, node, out);
+  }
 }
 
 // r = b - A x
@@ -541,14 +607,24 @@ template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, Op::MINB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ r) {
   TMG_PDL_ENTRY;
-  TMG_NODE_IDX
-  double out[DIM], self[DIM], bb[DIM];
-  load_node<DIM>(b, node, bb);  // in flight while the tile is staged
-  op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
-  if (!active) return;
+  if constexpr (Op::STREAM) {
+    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double*) {
+      double bb[DIM];
+      load_node<DIM>(b, node, bb);
 #pragma unroll
-  for (int c = 0; c < DIM; ++c) out[c] = bb[c] - out[c];
-  store_node<DIM>(r, node, out);
+      for (int c = 0; c < DIM; ++c) bb[c] -= o[c];
+      store_node<DIM>(r, node, bb);
+    });
+  } else {
+    TMG_NODE_IDX
+    double out[DIM], self[DIM], bb[DIM];
+    load_node<DIM>(b, node, bb);  // in flight while the tile is staged
+    op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
+    if (!active) return;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = bb[c] - out[c];
+    store_node<DIM>(r, node, out);
+  }
 }
 
 // xo = xs + w D^-1 (b - A xs)   (weighted Jacobi sweep, multigrid.py:57) where xs is
@@ -581,7 +657,24 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_jacobi(const __grid_constant_
                                                 const double* __restrict__ b, const double* __restrict__ dinv,
                                                 const double* __restrict__ wp, double* __restrict__ xo, Red red) {
   TMG_PDL_ENTRY;
-  jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
+  if constexpr (Op::STREAM) {
+    const double w = *wp;
+    double v = 0.0;
+    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double* self) {
+      double bb[DIM], d[DIM], out[DIM];
+      load_node<DIM>(b, node, bb);
+      load_node<DIM>(dinv, node, d);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        out[c] = self[c] + w * (d[c] * (bb[c] - o[c]));
+        if (DOT) v += out[c] * bb[c];
+      }
+      store_node<DIM>(xo, node, out);
+    });
+    if (DOT) grid_reduce(v, red);
+  } else {
+    jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
+  }
 }
 
 // first post-smoothing sweep with the coarse-grid correction fused in:
@@ -602,6 +695,24 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_bjacobi(const __grid_constant
                                                  const double* __restrict__ b, const double* __restrict__ binv,
                                                  const double* __restrict__ wp, double* __restrict__ xo) {
   TMG_PDL_ENTRY;
+  if constexpr (Op::STREAM) {
+    const double w = *wp;
+    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double* self) {
+      double r[DIM], out[DIM];
+      load_node<DIM>(b, node, r);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) r[c] -= o[c];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) s += binv[node * DIM * DIM + a * DIM + c] * r[c];
+        out[a] = self[a] + w * s;
+      }
+      store_node<DIM>(xo, node, out);
+    });
+    return;
+  }
   TMG_NODE_IDX
   double out[DIM], self[DIM], r[DIM];
   op.row(active, node, ci, cj, ck, VecSrc<DIM>{x}, out, self);
@@ -630,6 +741,29 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
                                               double* __restrict__ x, double* __restrict__ po,
                                               double* __restrict__ ro) {
   TMG_PDL_ENTRY;
+  if constexpr (Op::STREAM) {
+    const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
+    fine3_rows(op, ChebSrc<DIM>{zs, p, dinv, beta}, [&](int node, int, int, int, const double* o,
+                                                         const double* pv) {
+      double rr[DIM], xv[DIM];
+      load_node<DIM>(r, node, rr);
+      if (x_zero) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) xv[c] = 0.0;
+      } else {
+        load_node<DIM>(x, node, xv);
+      }
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        xv[c] += alpha * pv[c];
+        rr[c] -= alpha * o[c];
+      }
+      store_node<DIM>(po, node, pv);
+      store_node<DIM>(x, node, xv);
+      store_node<DIM>(ro, node, rr);
+    });
+    return;
+  }
   TMG_NODE_IDX
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
   double out[DIM], pv[DIM], rr[DIM], xv[DIM];

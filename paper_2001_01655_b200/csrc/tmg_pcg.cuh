@@ -47,6 +47,18 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__
                                                double* __restrict__ q, const CgState* __restrict__ st,
                                                const double* __restrict__ rz_new, Red red) {
   TMG_PDL_ENTRY;
+  if constexpr (Op::STREAM) {
+    const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
+    double v = 0.0;
+    fine3_rows(op, AxpySrc<DIM>{z, p, beta}, [&](int node, int, int, int, const double* o, const double* pv) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) v += pv[c] * o[c];
+      store_node<DIM>(pn, node, pv);
+      store_node<DIM>(q, node, o);
+    });
+    grid_reduce(v, red);
+    return;
+  }
   TMG_NODE_IDX
   const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
   double v = 0.0;
@@ -151,7 +163,7 @@ void pcg_prologue(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0, cudaS
   const unsigned gv = red_grid(n);
   auto op0 = K.template fine<DIM>();
   if (use_x0) {
-    launch(k_residual<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s, 
+    launch(k_residual<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), s, 
         op0, C.x.get(), C.b.get(),
                                                                                        C.r.get());
     note_launch();
@@ -188,7 +200,7 @@ void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGr
     launch(k_dot, gv, TPB, 0, s, C.r.get(), z, n, C.rz.red());
     note_launch();
   }
-  launch(k_cg_pq<DIM, decltype(op0)>, node_grid<DIM>(K.L), node_block<DIM>(), decltype(op0)::SMEM_BYTES, s, 
+  launch(k_cg_pq<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), s, 
       op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(), C.rz.res.get(), C.pq.red());
   launch(k_cg_update, gv, TPB, 0, s, C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
                                  C.pq.res.get(), C.rr.red(), z0 ? H->lv[0]->dinv.get() : nullptr,
@@ -290,7 +302,7 @@ PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy*
   bool rebuild = C.exec == nullptr || C.use_x0_graph != use_x0;
   if (C.ndof != n) {
     C.ndof = n;
-    const unsigned gmax = std::max(node_blocks(node_grid<DIM>(K.L)), 1184u);
+    const unsigned gmax = std::max({node_blocks(node_grid<DIM>(K.L)), node_blocks(row_grid<DIM, FineOp<DIM>>(K.L)), 1184u});
     cudaStream_t s = user;
     C.b.alloc(n, s); C.x.alloc(n, s); C.r.alloc(n, s); C.z.alloc(n, s);
     C.p.alloc(n, s); C.pn.alloc(n, s); C.q.alloc(n, s);
