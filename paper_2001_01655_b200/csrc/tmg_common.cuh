@@ -180,8 +180,13 @@ __device__ __forceinline__ double block_sum(double v) {
   return v;
 }
 
-// Every thread of every block must call this (uniform control flow).
-__device__ __forceinline__ void grid_reduce(double v, const Red& r) {
+// Every thread of every block must call this (uniform control flow).  fin(s)
+// runs once, in thread 0 of the last block, after the result is published.
+struct NoFinish {
+  __device__ void operator()(double) const {}
+};
+template <class Fin = NoFinish>
+__device__ __forceinline__ void grid_reduce(double v, const Red& r, Fin fin = Fin{}) {
   __shared__ bool last;
   const int t = lin_tid();
   const unsigned nb = lin_nblocks();
@@ -201,6 +206,7 @@ __device__ __forceinline__ void grid_reduce(double v, const Red& r) {
     if (t == 0) {
       *r.result = s;
       *r.counter = 0u;
+      fin(s);
     }
   }
 }

@@ -42,11 +42,15 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
 
 // p' = z + beta p (own node and, on the fly, its neighbours); q = A p'; reduce p'.q
 template <int DIM, class Op>
+// The search direction ping-pongs between P0 and P1 by iteration parity (no copy).
 __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
-                                               const double* __restrict__ p, double* __restrict__ pn,
+                                               double* __restrict__ P0, double* __restrict__ P1,
                                                double* __restrict__ q, const CgState* __restrict__ st,
                                                const double* __restrict__ rz_new, Red red) {
   TMG_PDL_ENTRY;
+  const bool odd = st->it & 1;
+  const double* __restrict__ p = odd ? P1 : P0;
+  double* __restrict__ pn = odd ? P0 : P1;
   if constexpr (Op::STREAM) {
     const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
     double v = 0.0;
@@ -73,15 +77,20 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__
   grid_reduce(v, red);
 }
 
-// x += alpha p'; r -= alpha q; p = p'; reduce r.r.  With z0: also the first
-// zero-start Jacobi sweep of the next V-cycle, z0 = w D0^-1 r.
-__global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
-                                                   const double* __restrict__ pn, const double* __restrict__ q,
+// x += alpha p'; r -= alpha q; reduce r.r, then (last block, on the reduced
+// r.r) the convergence check that drives the graph's WHILE node.  With z0: also the first zero-start Jacobi sweep of the
+// next V-cycle, z0 = w D0^-1 r.
+__global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, double* __restrict__ r,
+                                                   const double* __restrict__ P0, const double* __restrict__ P1,
+                                                   const double* __restrict__ q,
                                                    long long n, const double* __restrict__ rz_new,
                                                    const double* __restrict__ pq, Red red,
                                                    const double* __restrict__ dinv0, const double* __restrict__ wp0,
-                                                   double* __restrict__ z0) {
+                                                   double* __restrict__ z0, const CgCfg* __restrict__ cfg,
+                                                   CgState* __restrict__ st, double* __restrict__ hist,
+                                                   cudaGraphConditionalHandle h, int use_cond) {
   TMG_PDL_ENTRY;
+  const double* __restrict__ pn = (st->it & 1) ? P0 : P1;
   const double alpha = *rz_new / *pq;
   const double w0 = z0 ? *wp0 : 0.0;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -106,27 +115,21 @@ __global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, do
       x[i] = xv[u] + alpha * pv[u];
       const double ri = rv[u] - alpha * qv[u];
       r[i] = ri;
-      p[i] = pv[u];
       if (z0) z0[i] = w0 * (dv[u] * ri);
       v[u] += ri * ri;
     }
   }
-  grid_reduce((v[0] + v[1]) + (v[2] + v[3]), red);
-}
-
-__global__ void k_cg_check(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ rz_new,
-                           const double* __restrict__ rr, double* __restrict__ hist, cudaGraphConditionalHandle h,
-                           int use_cond) {
-  TMG_PDL_ENTRY;
-  st->rz = *rz_new;
-  const int it = st->it + 1;
-  st->it = it;
-  const double rn = sqrt(*rr);
-  hist[it] = rn;
-  const bool conv = rn <= st->tol;
-  st->converged = conv;
-  st->go = (!conv && it < cfg->maxit) ? 1 : 0;
-  if (use_cond) cudaGraphSetConditional(h, st->go ? 1u : 0u);
+  grid_reduce((v[0] + v[1]) + (v[2] + v[3]), red, [&](double rr) {
+    st->rz = *rz_new;
+    const int it = st->it + 1;
+    st->it = it;
+    const double rn = sqrt(rr);
+    hist[it] = rn;
+    const bool conv = rn <= st->tol;
+    st->converged = conv;
+    st->go = (!conv && it < cfg->maxit) ? 1 : 0;
+    if (use_cond) cudaGraphSetConditional(h, st->go ? 1u : 0u);
+  });
 }
 
 struct PcgCtx {
@@ -202,11 +205,11 @@ void pcg_body(PcgCtx& C, const Operator& K, Hierarchy* H, cudaStream_t s, cudaGr
   }
   launch(k_cg_pq<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), s, 
       op0, z, C.p.get(), C.pn.get(), C.q.get(), C.st.get(), C.rz.res.get(), C.pq.red());
-  launch(k_cg_update, gv, TPB, 0, s, C.x.get(), C.r.get(), C.p.get(), C.pn.get(), C.q.get(), n, C.rz.res.get(),
-                                 C.pq.res.get(), C.rr.red(), z0 ? H->lv[0]->dinv.get() : nullptr,
-                                 z0 ? H->lv[0]->wdev.get() : nullptr, z0);
-  launch(k_cg_check, 1, 1, 0, s, C.cfg.get(), C.st.get(), C.rz.res.get(), C.rr.res.get(), C.hist.get(), h, use_cond);
-  note_launch(3);
+  launch(k_cg_update, gv, TPB, 0, s, C.x.get(), C.r.get(), (const double*)C.p.get(), (const double*)C.pn.get(),
+         (const double*)C.q.get(), n, (const double*)C.rz.res.get(), (const double*)C.pq.res.get(), C.rr.red(),
+         z0 ? (const double*)H->lv[0]->dinv.get() : nullptr, z0 ? (const double*)H->lv[0]->wdev.get() : nullptr, z0,
+         (const CgCfg*)C.cfg.get(), C.st.get(), C.hist.get(), h, use_cond);
+  note_launch(2);
   TMG_CUDA(cudaGetLastError());
 }
 
