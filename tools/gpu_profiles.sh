@@ -6,7 +6,7 @@ R=${ROUND:-r01}
 timeout 900 python bench.py > gpurun_out/bench_$R.log 2>&1
 export TMG_PCG_EAGER=1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${NCU_C:-6000} --csv \
-  --log-file gpurun_out/launches_bench_$R.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline \
+  --log-file gpurun_out/launches_bench_$R.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --iters-cap 50 --e2e-steps 1 \
   > gpurun_out/ncu_bench_$R.log 2>&1
 for spec in "fine_jacobi:_ZN3tmg8k_jacobiILi2ENS_6FineOpILi2EEELb0EEEvT0_PKdS5_S5_S5_PdNS_3RedE:gmg:4" \
             "fine_jacobi_dot:_ZN3tmg8k_jacobiILi2ENS_6FineOpILi2EEELb1EEEvT0_PKdS5_S5_S5_PdNS_3RedE:gmg:2" \
