@@ -261,10 +261,23 @@ void sor_setup(Level& l, cudaStream_t s, DevBuf<unsigned>& bad) {
 inline void sor_solve(const Level& l, const double* v, double* z, cudaStream_t s) {
   const Bsr& A = sor_matrix(l);
   launch(k_sor_prep, 1, 1, 0, s, l.sor_ctl.get());
+  static const int sleep_ns = [] {
+    const char* e = std::getenv("TMG_SOR_SLEEP");
+    return e ? std::max(0, std::atoi(e)) : 64;
+  }();
+  static const int acquire = [] {
+    const char* e = std::getenv("TMG_SOR_ACQUIRE");
+    return e ? std::atoi(e) : 1;
+  }();
   const SorView S{A.rowptr.get(), A.col.get(), A.val.get(), l.sor_diag.get(), l.sor_order.get(), A.nrows,
-                  l.sor_flag.get(), l.sor_ctl.get()};
-  // a few hundred rows per level set are ready at a time: 4 warps per SMSP suffice
-  const unsigned grid = (unsigned)std::min<long long>(((long long)A.nrows * 32 + SOR_TPB - 1) / SOR_TPB, 148 * 2);
+                  l.sor_flag.get(), l.sor_ctl.get(), sleep_ns, acquire};
+  // Only a few level sets' worth of rows can be ready at a time; more resident
+  // warps only add flag polls to the L2 (TMG_SOR_CTAS overrides, A/B)
+  static const int ctas = [] {
+    const char* e = std::getenv("TMG_SOR_CTAS");
+    return e ? std::max(1, std::atoi(e)) : 148 * 2;
+  }();
+  const unsigned grid = (unsigned)std::min<long long>(((long long)A.nrows * 32 + SOR_TPB - 1) / SOR_TPB, ctas);
   TMG_BSR_SQUARE_DISPATCH(A.R, launch(k_sor_solve<RR>, grid, SOR_TPB, 0, s, S, v, z))
   note_launch(2);
 }

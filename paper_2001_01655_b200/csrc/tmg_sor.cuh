@@ -27,11 +27,21 @@ struct SorView {
   int nrows;
   int* flag;  // per block row: epoch of the last solve that finished it
   int* ctl;   // [0] epoch, [1] ticket counter
+  int sleep_ns;  // poll back-off cap (0: spin)
+  int acquire;   // 1: acquire once per observed dependency (z is read through L2 either way)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Polls use relaxed loads: an acquire load also invalidates the SM's L1, and
+// with hundreds of polling warps per SM that evicts every row's prefetched
+// blocks.  Only the final, successful observation is an acquire.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -50,6 +60,11 @@ constexpr int SOR_TPB = 256;
 template <int R>
 __global__ void __launch_bounds__(SOR_TPB) k_sor_solve(SorView S, const double* __restrict__ v, double* z) {
   TMG_PDL_ENTRY;
+  // Everything a row needs that does not depend on other rows (its right-hand
+  // side, diagonal block and, for R <= 3, its lower blocks) is loaded BEFORE the
+  // row waits on its dependencies, so a dependency hop costs one flag
+  // observation + one z load + the arithmetic + one release store.
+  constexpr bool PRE = R <= 3;
   const int lane = threadIdx.x & 31;
   const int epoch = *(volatile int*)S.ctl;
   while (true) {
@@ -59,41 +74,58 @@ __global__ void __launch_bounds__(SOR_TPB) k_sor_solve(SorView S, const double* 
     if (t >= S.nrows) return;
     const int row = S.order[t];
     const int beg = S.rowptr[row], dp = S.diagpos[row];
+    double D[PRE ? R * R : 1], vr[R];
+    if (lane == 0) {
+#pragma unroll
+      for (int a = 0; a < R; ++a) vr[a] = v[(long long)row * R + a];
+      if constexpr (PRE) {
+#pragma unroll
+        for (int q = 0; q < R * R; ++q) D[q] = __ldg(S.val + (long long)dp * R * R + q);
+      }
+    }
     double acc[R];
 #pragma unroll
     for (int a = 0; a < R; ++a) acc[a] = 0.0;
     for (int p = beg + lane; p < dp; p += 32) {
       const int j = S.col[p];
-      if (ld_acquire(S.flag + j) != epoch) {
-        // back off: thousands of spinning warps would otherwise saturate L2 with polls
-        unsigned ns = 32;
-        do {
-          __nanosleep(ns);
-          ns = ns < 256 ? 2 * ns : ns;
-        } while (ld_acquire(S.flag + j) != epoch);
+      const double* blk = S.val + (long long)p * R * R;
+      double bv[PRE ? R * R : 1];
+      if constexpr (PRE) {
+#pragma unroll
+        for (int q = 0; q < R * R; ++q) bv[q] = __ldg(blk + q);
       }
+      if (ld_relaxed(S.flag + j) != epoch) {
+        // optional back-off: many spinning warps can saturate the L2 with polls
+        unsigned ns = 8;
+        do {
+          if (S.sleep_ns) {
+            __nanosleep(ns);
+            ns = ns < (unsigned)S.sleep_ns ? 2 * ns : ns;
+          }
+        } while (ld_relaxed(S.flag + j) != epoch);
+      }
+      if (S.acquire) (void)ld_acquire(S.flag + j);
       double zj[R];
 #pragma unroll
       for (int b = 0; b < R; ++b) zj[b] = __ldcg(z + (long long)j * R + b);
-      const double* blk = S.val + (long long)p * R * R;
 #pragma unroll
       for (int a = 0; a < R; ++a)
 #pragma unroll
-        for (int b = 0; b < R; ++b) acc[a] += __ldg(blk + a * R + b) * zj[b];
+        for (int b = 0; b < R; ++b) acc[a] += (PRE ? bv[a * R + b] : __ldg(blk + a * R + b)) * zj[b];
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
       for (int a = 0; a < R; ++a) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off);
     if (lane == 0) {
-      const double* D = S.val + (long long)dp * R * R;
+      const double* Dg = S.val + (long long)dp * R * R;
       double zi[R];
 #pragma unroll
       for (int a = 0; a < R; ++a) {
-        double s = v[(long long)row * R + a] - acc[a];
+        double s = vr[a] - acc[a];
 #pragma unroll
-        for (int b = 0; b < a; ++b) s -= D[a * R + b] * zi[b];
-        zi[a] = s / D[a * R + a];
+        for (int b = 0; b < a; ++b) s -= (PRE ? D[a * R + b] : Dg[a * R + b]) * zi[b];
+        zi[a] = s / (PRE ? D[a * R + a] : Dg[a * R + a]);
         z[(long long)row * R + a] = zi[a];
       }
       st_release(S.flag + row, epoch);
