@@ -64,10 +64,15 @@ typedef struct {
                         device pointer, copied during the build */
 } tmg_smoother_desc;
 
-/* SolveConfig (krylov.py:17) for the preconditioned CG extension. */
+/* SolveConfig (krylov.py:17).  tmg_pcg_solve reads rtol / max_iterations; the
+ * host-buffer entry tmg_solve_compliance_host also dispatches on method like
+ * krylov.solve (krylov.py:146): 0 CG (extension, zero-initialised default),
+ * 1 gmres_solve, 2 fgmres_solve, with restart (<= 0: the reference's 200). */
 typedef struct {
   double rtol;            /* ||r|| <= rtol * ||b||, as krylov.py:63 */
   int32_t max_iterations;
+  int32_t method;
+  int32_t restart;
 } tmg_solve_desc;
 
 /* SolveRecord (krylov.py:31). */

@@ -22,7 +22,8 @@ class SmootherDesc(C.Structure):
 
 
 class SolveDesc(C.Structure):
-    _fields_ = [("rtol", C.c_double), ("max_iterations", C.c_int32)]
+    _fields_ = [("rtol", C.c_double), ("max_iterations", C.c_int32), ("method", C.c_int32),
+                ("restart", C.c_int32)]
 
 
 class GmresDesc(C.Structure):

@@ -716,7 +716,14 @@ int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
                           mg->beta, mg->v0_host, &mg->smoother, mg->n_pre, mg->n_post, mg->isolated_mode, s, &H);
   if (rc) return rc;
   std::unique_ptr<tmg_hierarchy> Hg(H);
-  rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);
+  TMG_REQUIRE(cfg->method >= 0 && cfg->method <= 2, "unknown Krylov method");
+  if (cfg->method == 0) {
+    rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);
+  } else {
+    const tmg_gmres_desc g{cfg->rtol, cfg->max_iterations, cfg->restart > 0 ? cfg->restart : 200,
+                           cfg->method == 2 ? 1 : 0};
+    rc = tmg_gmres_solve(K, H, f.get(), u.get(), 0, &g, nullptr, rec, s);
+  }
   if (rc) return rc;
   rc = tmg_compliance_sensitivity(K, rho.get(), f.get(), u.get(), penalty, e0, emin, dc.get(), compliance_host, s);
   if (rc) return rc;
