@@ -174,3 +174,32 @@ def test_full_size_config2_four_load_cases_share_one_hierarchy():
         assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(f)  # true residual (recursive one: 1e-8)
         sols.append(host(u))
     assert all(np.isfinite(u).all() for u in sols)
+
+
+def test_full_size_config1_pcg_trajectories_match_oracle():
+    """The bench workload itself, both legs, 2000 PCG iterations, against the
+    oracle's run on the same input (tests/golden/make_config1_history.py): same
+    hierarchy sizes, the same early residual trajectory, and the same failure
+    mode at the cap (neither reaches rtol 1e-8 on this non-percolating density,
+    DESIGN.md deviation 7).  The early agreement is limited by the coarsest
+    operators (GMG: 2562 dofs, cond 4.6e13), whose direct solves differ in
+    forward error at the percent level between any two implementations
+    (device explicit inverse vs scipy splu, tools/coarse_check.py)."""
+    import os
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "config1_history.npz"))
+    w, E = workload(1)
+    K = T.assemble_stiffness(w.mesh, w.bc, E)
+    for leg in w.solvers:
+        tag = "gmg" if leg["strategy"] == "gmg" else "amg"
+        h = LegRunner(w, leg).build(K)
+        assert [lv.size for lv in h.levels] == list(ref[tag + "_sizes"]), tag
+        u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=2000))
+        hist = np.array(rec.residual_history)
+        rh = ref[tag + "_hist"]
+        assert len(hist) == len(rh) == 2001, tag
+        d = np.abs(hist - rh) / rh
+        print(tag, "rel. diff of the first 12 residuals", np.array2string(d[:12], precision=3),
+              "final rel. residual gpu %.3e oracle %.3e" % (hist[-1] / hist[0], rh[-1] / rh[0]))
+        assert d[:11].max() <= 0.1, (tag, d[:11])
+        assert not rec.converged and rh[-1] / rh[0] > w.rtol
+        assert 0.1 <= (hist[-1] / hist[0]) / (rh[-1] / rh[0]) <= 10.0, tag
