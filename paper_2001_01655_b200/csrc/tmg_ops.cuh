@@ -233,11 +233,14 @@ struct FineOp {
   static constexpr int EX = BX + 1, EY = BY + 1, EZ = DIM == 2 ? 1 : BZ + 1;
   static constexpr int NH = HX * HY * HZ, NEL = EX * EY * EZ;
   static constexpr size_t SMEM_BYTES = sizeof(double) * (NH * DIM + NEL) + NH;
-  // resident blocks per SM the register budget is sized for (2D: 64 regs)
+  // resident blocks per SM the register budget is sized for (2D: 48 regs, 3D: 80)
 #ifndef TMG_F3_MINB
 #define TMG_F3_MINB 3  // 3D: 80 registers, 3 CTAs per SM (measured best of 2/3/4)
 #endif
-  static constexpr int MINB = DIM == 2 ? 4 : TMG_F3_MINB;
+#ifndef TMG_F2_MINB
+#define TMG_F2_MINB 5  // 2D: 48 registers, 5 CTAs per SM (measured: sweep 5.82 -> 5.45 us vs 4 / 6 CTAs)
+#endif
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
   // 3D pair rows (tmg_fine3.cuh, fine3_rows: two x-adjacent nodes per thread)
   // are an A/B build option (-DTMG_FINE3_PAIR); measured on par with the tile
   // (201 vs 194 us per config-4 sweep), so the tile stays the default.
