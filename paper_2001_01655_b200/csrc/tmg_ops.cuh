@@ -482,7 +482,10 @@ struct StencilOp {
   // batch before any arithmetic) so a thread has G*(DD+DIM) loads in flight --
   // coarse levels have too few threads to hide L2 latency by occupancy alone.
   static constexpr size_t SMEM_BYTES = 0;
-  static constexpr int MINB = 1;  // full register budget: batched loads in flight
+#ifndef TMG_ST_MINB
+#define TMG_ST_MINB 2  // 3D stencil rows: 128 instead of 254 registers (config-3 PCG 370.8 -> 355.7 us/iter; 3 / 4: slower)
+#endif
+  static constexpr int MINB = TMG_ST_MINB;  // large register budget: batched loads in flight
   static constexpr bool STREAM = false;
   template <class Src>
   __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
