@@ -32,7 +32,10 @@ struct SmootherCfg {
 // ----------------------------------------------------------------------------
 // Reduction kernels run on a small grid (RED_BLOCKS) with 4 independent loads in
 // flight per thread, so the last-block combine reads few partials.
-constexpr unsigned RED_BLOCKS = 296;  // 2 per SM
+#ifndef TMG_RED_BLOCKS
+#define TMG_RED_BLOCKS 296
+#endif
+constexpr unsigned RED_BLOCKS = TMG_RED_BLOCKS;  // 2 per SM
 inline unsigned red_grid(long long n) { return std::min<unsigned>(grid_for(n), RED_BLOCKS); }
 
 __global__ void __launch_bounds__(TPB) k_dot(const double* __restrict__ a, const double* __restrict__ b, long long n,
