@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 F8 = 8
+FP64_PEAK_TF = 37.0  # B200 dense FP64 (vector) peak, NVIDIA datasheet figure (not measured here)
 
 
 def level_bytes(h, k, ndim, mesh, n_levels):
@@ -98,10 +99,18 @@ def main():
                     phases.append((nm, by, ms.value))
             for nm, by, t in phases:
                 gbs = by / (t * 1e-3) / 1e9 if t > 0 else 0.0
-                rows.append(dict(leg=lr.name, level=k, storage=lv.storage, dofs=lv.size, phase=nm, bytes=by,
-                                 us=t * 1e3, gbs=gbs, frac=gbs / peak))
-                print("  %-6s %3d %-11s %9d  %-9s %10d %8.2f %9.0f %6.2f" % (lr.name, k, lv.storage, lv.size, nm, by,
-                                                                           t * 1e3, gbs, gbs / peak), flush=True)
+                row = dict(leg=lr.name, level=k, storage=lv.storage, dofs=lv.size, phase=nm, bytes=by,
+                           us=t * 1e3, gbs=gbs, frac=gbs / peak)
+                extra = ""
+                if lv.storage == "matrix_free" and w.mesh.ndim == 3 and nm in ("sweep", "residual"):
+                    # the Hex8 operator is FP64-bound: 576 FMA per node (24x24 KE per element)
+                    tf = 2.0 * 576 * w.mesh.node_count / (t * 1e-3) / 1e12
+                    row.update(fp64_tflops=tf, fp64_frac=tf / FP64_PEAK_TF)
+                    extra = "   FP64 %.1f TF/s = %.2f of %.0f" % (tf, tf / FP64_PEAK_TF, FP64_PEAK_TF)
+                rows.append(row)
+                print("  %-6s %3d %-11s %9d  %-9s %10d %8.2f %9.0f %6.2f%s" % (lr.name, k, lv.storage, lv.size, nm, by,
+                                                                             t * 1e3, gbs, gbs / peak, extra),
+                      flush=True)
     json.dump(rows, open(os.path.join(ROOT, "gpurun_out", "roofline_c%d.json" % a.config), "w"), indent=1)
 
 
