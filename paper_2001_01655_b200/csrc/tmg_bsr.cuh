@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_cheb(BsrView<R, R> A, const double*
   for (int a = 0; a < R; ++a) {
     const long long i = (long long)row * R + a;
     x[i] = (x_zero ? 0.0 : x[i]) + alpha * pn[i];
-    ro[i] = r[i] - alpha * out[a];
+    if (ro) ro[i] = r[i] - alpha * out[a];
   }
 }
 

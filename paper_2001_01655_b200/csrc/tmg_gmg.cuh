@@ -597,7 +597,8 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
         zs = l.z.get();
         dv = nullptr;
       }
-      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, ro, s);
+      // the last step's r' is never read (the next pass starts from b - A x)
+      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, i + 1 < H.sm.degree ? ro : nullptr, s);
       rin = ro;
       pin = po;
     }

@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
       }
       store_node<DIM>(po, node, pv);
       store_node<DIM>(x, node, xv);
-      store_node<DIM>(ro, node, rr);
+      if (ro) store_node<DIM>(ro, node, rr);
     });
     return;
   }
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
   }
   store_node<DIM>(po, node, pv);
   store_node<DIM>(x, node, xv);
-  store_node<DIM>(ro, node, rr);
+  if (ro) store_node<DIM>(ro, node, rr);  // nullptr: last step of a pass, r' is never read
 }
 
 // diagonal / nodal block inverses of a level operator
