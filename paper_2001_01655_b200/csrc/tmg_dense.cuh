@@ -237,36 +237,46 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const double* __restrict__ A,
   t = warp_sum(t);
   if (lane == 0) y[row] = t;
 }
-// Even n (rows 16-byte aligned): 128-bit loads, 16 row doubles in flight per lane
-// (the coarsest inverse is 52 MB on config 1; one warp per row leaves only ~17
-// warps per SM, so bytes in flight per warp decide the bandwidth).
-__global__ void __launch_bounds__(256) k_gemv_rows2(const double* __restrict__ A, long long n,
-                                                    const double* __restrict__ b, double* __restrict__ y) {
+// Even n (rows 16-byte aligned): one row per block of S warps (split-K), 128-bit
+// loads; S x the bytes in flight of a warp-per-row kernel (2562 rows leave only
+// ~17 warps per SM otherwise, the coarsest inverse is 52 MB on config 1).  The
+// S partial sums are combined in a fixed order (deterministic).
+template <int S>
+__global__ void __launch_bounds__(32 * S) k_gemv_split(const double* __restrict__ A, long long n,
+                                                      const double* __restrict__ b, double* __restrict__ y) {
   TMG_PDL_ENTRY;
-  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
+  __shared__ double part[S];
+  const long long row = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* a = reinterpret_cast<const double2*>(A + row * n);
   const double2* bb = reinterpret_cast<const double2*>(b);
   const long long n2 = n >> 1;
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long j = lane;
-  for (; j + 7 * 32 < n2; j += 8 * 32) {
-    double2 av[8], bv[8];
+  double s[4] = {0, 0, 0, 0};
+  long long j = threadIdx.x;
+  constexpr int T = 32 * S;
+  for (; j + 3 * T < n2; j += 4 * T) {
+    double2 av[4], bv[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) av[u] = __ldg(a + j + 32 * u);
+    for (int u = 0; u < 4; ++u) av[u] = __ldg(a + j + T * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) bv[u] = __ldg(bb + j + 32 * u);
+    for (int u = 0; u < 4; ++u) bv[u] = __ldg(bb + j + T * u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] += av[u].x * bv[u].x + av[u].y * bv[u].y;
+    for (int u = 0; u < 4; ++u) s[u] += av[u].x * bv[u].x + av[u].y * bv[u].y;
   }
-  for (int u = 0; j < n2; j += 32, ++u) {
+  for (int u = 0; j < n2; j += T, ++u) {
     const double2 av = __ldg(a + j), bv = __ldg(bb + j);
-    s[u & 7] += av.x * bv.x + av.y * bv.y;
+    s[u & 3] += av.x * bv.x + av.y * bv.y;
   }
-  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  double t = (s[0] + s[1]) + (s[2] + s[3]);
   t = warp_sum(t);
-  if (lane == 0) y[row] = t;
+  if (lane == 0) part[w] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q) r += part[q];
+    y[row] = r;
+  }
 }
 
 // TMG_DENSE_MMA=0 selects the CUDA-core update (A/B switch and parity check).
@@ -305,8 +315,10 @@ struct DenseInverse {
     D.release();
   }
   void apply(const double* b, double* y, cudaStream_t s) const {
+    // measured on config 1's 2562-row inverse: split-K 4 warps 9.3 us, warp per
+    // row 11.5 us, 8 warps 12.7 us
     if ((n & 1) == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0)
-      launch(k_gemv_rows2, grid_for(n * 32), 256, 0, s, A.get(), n, b, y);
+      launch(k_gemv_split<4>, (unsigned)n, 128, 0, s, A.get(), n, b, y);
     else
       launch(k_gemv_rows, grid_for(n * 32), 256, 0, s, A.get(), n, b, y);
     ::tmg::note_launch();
