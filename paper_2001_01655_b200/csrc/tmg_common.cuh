@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
@@ -210,6 +212,26 @@ __device__ __forceinline__ void grid_reduce(double v, const Red& r, Fin fin = Fi
     }
   }
 }
+
+// Setup phase timer (TMG_VERBOSE=1: synchronises and prints per phase).
+struct PhaseLog {
+  bool on = false;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseLog(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("TMG_VERBOSE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, long long a = -1) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tmg] %-28s %9.3f ms  %lld\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count(), a);
+    t0 = t;
+  }
+};
 
 // A reduction slot with its own storage.
 struct RedSlot {

@@ -556,13 +556,17 @@ std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dof
   DevBuf<unsigned> bad;
   bad.alloc(1, s);
   bad.zero(s);
+  PhaseLog log(s);
   auto plan = gmg_plan(DIM, K.ne, coarse_max_dofs, max_levels);
   H->lv.push_back(fine_level<DIM>(K));
   H->provenance.push_back(0);
   add_geometric_levels<DIM>(*H, plan, s);
+  log.mark("gmg: Galerkin stencils");
   const int nl = (int)H->lv.size();
   for (int k = 0; k < nl; ++k) level_setup<DIM>(*H, *H->lv[k], k < nl - 1, s, bad);
+  log.mark("gmg: smoother setup");
   coarse_setup<DIM>(*H, s);
+  log.mark("gmg: coarse inverse (n)", H->coarse.n);
   finalize_checks(*H, bad, s);
   return H;
 }

@@ -13,24 +13,6 @@
 namespace tmg {
 
 // TMG_VERBOSE=1: per-phase setup timings on stderr (synchronises the stream).
-struct PhaseLog {
-  bool on = false;
-  cudaStream_t s;
-  std::chrono::steady_clock::time_point t0;
-  explicit PhaseLog(cudaStream_t st) : s(st) {
-    const char* e = std::getenv("TMG_VERBOSE");
-    on = e && e[0] == '1';
-    t0 = std::chrono::steady_clock::now();
-  }
-  void mark(const char* what, long long a = -1) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[tmg] %-28s %9.3f ms  %lld\n", what,
-                 std::chrono::duration<double, std::milli>(t - t0).count(), a);
-    t0 = t;
-  }
-};
 
 __global__ void k_sqrt_to(const double* __restrict__ v2, double* __restrict__ out) {
   TMG_PDL_ENTRY; *out = sqrt(*v2); }
@@ -463,12 +445,15 @@ std::unique_ptr<Hierarchy> build_sa_amg(const Operator& K, const double* B_dev, 
   H->lv.push_back(fine_level<DIM>(K));
   H->provenance.push_back(1);
   sa_levels<DIM>(*H, B_dev, nvec, bs, coarse_max_dofs, beta, v0, s);
+  PhaseLog log(s);
   DevBuf<unsigned> bad;
   bad.alloc(1, s);
   bad.zero(s);
   const int nl = (int)H->lv.size();
   for (int k = 0; k < nl; ++k) level_setup<DIM>(*H, *H->lv[k], k < nl - 1, s, bad);
+  log.mark("sa: smoother setup");
   coarse_setup<DIM>(*H, s);
+  log.mark("sa: coarse inverse (n)", H->coarse.n);
   finalize_checks(*H, bad, s);
   return H;
 }
