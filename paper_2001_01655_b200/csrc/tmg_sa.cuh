@@ -167,7 +167,7 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool dr
   note_launch(3);
   // pass 1: distance-2 LFMIS (cooperative rounds)
   DevBuf<int> st, flag, rounds;
-  st.alloc(n, s); flag.alloc(1, s); flag.zero(s); rounds.alloc(1, s);
+  st.alloc(n, s); flag.alloc(1, s); flag.zero(s); rounds.alloc(1, s); rounds.zero(s);
   k_agg_init<<<grid_for(n), TPB, 0, s>>>(l.sptr.get(), n, st.get());
   {
     // flat lower-numbered distance-2 lists (count, scan, fill)
@@ -195,7 +195,7 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool dr
     lg.mark("  strength graph (nnz)", snnz);
     TMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis2, blocks, TPB, args, 0, s));
     note_launch();
-    if (lg.on) lg.mark("  LFMIS (rounds)", read_int(rounds.get(), s));
+    if (lg.on) lg.mark("  LFMIS (max sweeps)", read_int(rounds.get(), s));
   }
   DevBuf<int> isroot, rank, agg1, ptr, isoflag, isorank;
   isroot.alloc(n + 1, s); rank.alloc(n + 1, s); agg1.alloc(n, s); ptr.alloc(n, s);
