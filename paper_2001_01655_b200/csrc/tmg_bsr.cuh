@@ -74,10 +74,24 @@ __device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lan
 #pragma unroll
       for (int b = 0; b < C; ++b) xv[b] = __ldg(x + (long long)j * C + b);
       const double* blk = A.val + (long long)p * R * C;
+      if constexpr ((R * C) % 2 == 0) {  // 16-byte aligned blocks: 128-bit loads
+        double bv[R * C];
 #pragma unroll
-      for (int a = 0; a < R; ++a)
+        for (int q = 0; q < R * C / 2; ++q) {
+          const double2 t2 = __ldg(reinterpret_cast<const double2*>(blk) + q);
+          bv[2 * q] = t2.x;
+          bv[2 * q + 1] = t2.y;
+        }
 #pragma unroll
-        for (int b = 0; b < C; ++b) out[a] += __ldg(blk + a * C + b) * xv[b];
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < C; ++b) out[a] += bv[a * C + b] * xv[b];
+      } else {
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < C; ++b) out[a] += __ldg(blk + a * C + b) * xv[b];
+      }
     }
   }
   for (int off = (1 << A.gshift) >> 1; off > 0; off >>= 1)
