@@ -72,7 +72,17 @@ __device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lan
       const int j = A.col[p];
       double xv[C];
 #pragma unroll
-      for (int b = 0; b < C; ++b) xv[b] = __ldg(x + (long long)j * C + b);
+      for (int b = 0; b < C; ++b) {
+        if constexpr (C % 2 == 0) {  // 16-byte aligned node values
+          if (b % 2 == 0) {
+            const double2 t2 = __ldg(reinterpret_cast<const double2*>(x + (long long)j * C + b));
+            xv[b] = t2.x;
+            xv[b + 1] = t2.y;
+          }
+        } else {
+          xv[b] = __ldg(x + (long long)j * C + b);
+        }
+      }
       const double* blk = A.val + (long long)p * R * C;
       if constexpr ((R * C) % 2 == 0) {  // 16-byte aligned blocks: 128-bit loads
         double bv[R * C];
