@@ -17,6 +17,9 @@ struct Bsr {
   long long nnzb = 0;
   DevBuf<int> rowptr, col;
   DevBuf<double> val;
+  // 3x3 blocks padded to 10 doubles (16-byte aligned, 128-bit loads) for the
+  // V-cycle row kernels; made once the hierarchy is built (pad_blocks)
+  DevBuf<double> vpad;
   long long scalar_nnz() const { return nnzb * R * C; }
 };
 
@@ -27,6 +30,7 @@ struct BsrView {
   const double* __restrict__ val;
   int nrows;
   int gshift;  // 2^gshift lanes cooperate on one block row (row kernels below)
+  const double* __restrict__ vpad;  // R*C odd: padded copy (stride R*C+1) or nullptr
 };
 // Lanes per block row: the largest power of two <= half the mean blocks per row
 // (<= 32).  The coarse Galerkin levels carry 15-60 blocks per row, where one
@@ -41,7 +45,7 @@ inline int bsr_gshift(int nrows, long long nnzb) {
 }
 template <int R, int C>
 inline BsrView<R, C> view(const Bsr& m) {
-  return BsrView<R, C>{m.rowptr.get(), m.col.get(), m.val.get(), m.nrows, bsr_gshift(m.nrows, m.nnzb)};
+  return BsrView<R, C>{m.rowptr.get(), m.col.get(), m.val.get(), m.nrows, bsr_gshift(m.nrows, m.nnzb), m.vpad.get()};
 }
 // grid of a row kernel on m (threads = rows << gshift)
 inline unsigned bsr_grid(const Bsr& m) {
@@ -89,6 +93,20 @@ __device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lan
 #pragma unroll
         for (int q = 0; q < R * C / 2; ++q) {
           const double2 t2 = __ldg(reinterpret_cast<const double2*>(blk) + q);
+          bv[2 * q] = t2.x;
+          bv[2 * q + 1] = t2.y;
+        }
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+#pragma unroll
+          for (int b = 0; b < C; ++b) out[a] += bv[a * C + b] * xv[b];
+      } else if (A.vpad) {  // padded odd blocks: stride R*C+1 doubles, 16-byte aligned
+        constexpr int S2 = (R * C + 1) / 2;
+        double bv[2 * S2];
+        const double2* b2 = reinterpret_cast<const double2*>(A.vpad + (long long)p * (R * C + 1));
+#pragma unroll
+        for (int q = 0; q < S2; ++q) {
+          const double2 t2 = __ldg(b2 + q);
           bv[2 * q] = t2.x;
           bv[2 * q + 1] = t2.y;
         }
@@ -276,6 +294,23 @@ __global__ void k_bsr_to_dense(BsrView<R, R> A, double* __restrict__ Ad, long lo
       for (int b = 0; b < R; ++b)
         Ad[((long long)row * R + a) * n + (long long)j * R + b] = A.val[(long long)p * R * R + a * R + b];
   }
+}
+
+__global__ void k_bsr_pad(const double* __restrict__ val, long long nnzb, int rc, double* __restrict__ vp) {
+  TMG_PDL_ENTRY;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= nnzb * (rc + 1)) return;
+  const long long p = i / (rc + 1);
+  const int q = (int)(i - p * (rc + 1));
+  vp[i] = q < rc ? val[p * rc + q] : 0.0;
+}
+// padded V-cycle copy of an odd-block-size BSR (no-op otherwise)
+inline void bsr_pad_blocks(Bsr& m, cudaStream_t s) {
+  const int rc = m.R * m.C;
+  if (rc % 2 == 0 || m.nnzb == 0 || m.vpad.get()) return;
+  m.vpad.alloc(m.nnzb * (rc + 1), s);
+  launch(k_bsr_pad, grid_for(m.nnzb * (rc + 1)), TPB, 0, s, (const double*)m.val.get(), m.nnzb, rc, m.vpad.get());
+  note_launch();
 }
 
 // Dispatch helpers over the block shapes used by SA-AMG (dpn in {2,3}, nvec in {3,6}).

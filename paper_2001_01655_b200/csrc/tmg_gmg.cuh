@@ -465,7 +465,17 @@ void coarse_setup(Hierarchy& H, cudaStream_t s) {
   H.coarse.build(s);
 }
 
+// padded copies of the odd-block algebraic operators for the V-cycle row kernels
+// (after every setup kernel that indexes the unpadded values); TMG_BSR_PAD=0: off
+inline void pad_cycle_operators(Hierarchy& H, cudaStream_t s) {
+  const char* e = std::getenv("TMG_BSR_PAD");
+  if (e && e[0] == '0') return;
+  for (auto& lp : H.lv)
+    if (!lp->lattice()) bsr_pad_blocks(lp->Ab, s);
+}
+
 inline void finalize_checks(Hierarchy& H, DevBuf<unsigned>& bad, cudaStream_t s) {
+  pad_cycle_operators(H, s);
   unsigned hbad = 0, cbad = 0;
   TMG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   TMG_CUDA(cudaMemcpyAsync(&cbad, H.coarse.bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
