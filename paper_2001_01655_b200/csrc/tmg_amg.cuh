@@ -193,6 +193,50 @@ __global__ void k_lfmis2(const int* __restrict__ n2ptr, const int* __restrict__ 
   (void)last_undecided_round;
 }
 
+// Rounds of the distance-2 LFMIS in one cooperative launch, over the flat
+// lists (8 states in flight per thread per step).  A node becomes a MEMBER if a
+// lower-numbered node within distance 2 is a ROOT, a ROOT if none of them is
+// still undecided.  Decisions are final and monotone, so reading neighbours'
+// states while they are being written only changes WHEN a node decides, never
+// WHAT it decides (the result is the sequential greedy MIS of multigrid.py:380).
+__global__ void k_lfmis2_rounds(const int* __restrict__ n2ptr, const int* __restrict__ n2col, int n, int* st,
+                         int* __restrict__ last_undecided_round, int* __restrict__ rounds_out) {
+  TMG_PDL_ENTRY;
+  cg::grid_group grid = cg::this_grid();
+  volatile int* vst = st;
+  const int stride = gridDim.x * blockDim.x;
+  for (int round = 1;; ++round) {
+    bool pending = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      if (vst[i] != ST_UND) continue;
+      const int b = n2ptr[i], e = n2ptr[i + 1];
+      bool root_near = false, und_near = false;
+      for (int p = b; p < e && !root_near; p += 8) {
+        int kk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kk[u] = p + u < e ? __ldg(n2col + p + u) : -1;
+        int sv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sv[u] = kk[u] >= 0 ? vst[kk[u]] : ST_MEMBER;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          root_near |= sv[u] == ST_ROOT;
+          und_near |= sv[u] == ST_UND;
+        }
+      }
+      if (root_near) vst[i] = ST_MEMBER;
+      else if (!und_near) vst[i] = ST_ROOT;
+      else pending = true;
+    }
+    if (pending) atomicMax(last_undecided_round, round);
+    grid.sync();
+    if (*(volatile int*)last_undecided_round < round) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *rounds_out = round;
+      return;
+    }
+  }
+}
+
 // pass-1 aggregate ids: roots by rank; members by their adjacent root; -1 isolated; -2 leftover
 __global__ void k_agg_pass1(const int* __restrict__ sptr, const int* __restrict__ scol, int n,
                             const int* __restrict__ st, const int* __restrict__ rank, int* __restrict__ agg) {

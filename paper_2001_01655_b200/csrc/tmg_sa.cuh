@@ -183,7 +183,20 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool dr
     int dev = 0, nsm = 0, per = 0;
     TMG_CUDA(cudaGetDevice(&dev));
     TMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    TMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lfmis2, TPB, 0));
+    // Barrier-free sweeps win while a thread owns ~1 node (config 1 level 0:
+    // 3.4 vs 6.4 ms); with several nodes per thread every re-sweep gets longer
+    // and grid-synchronised rounds win (config 2 level 0: 13.2 vs 20.1 ms).
+    // TMG_LFMIS_ASYNC=0/1 forces one of them.
+    static const int force = [] {
+      const char* e = std::getenv("TMG_LFMIS_ASYNC");
+      return e ? std::atoi(e) : -1;
+    }();
+    int per_a = 0, per_r = 0;
+    TMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_a, k_lfmis2, TPB, 0));
+    TMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_r, k_lfmis2_rounds, TPB, 0));
+    const bool async = force >= 0 ? force == 1 : (long long)n <= 2LL * nsm * per_a * TPB;
+    void* kfun = async ? (void*)k_lfmis2 : (void*)k_lfmis2_rounds;
+    per = async ? per_a : per_r;
     const int blocks = std::max(1, std::min(nsm * per, (int)grid_for(n)));
     const int* a0 = n2ptr.get();
     const int* a1 = n2col.get();
@@ -193,7 +206,7 @@ inline void aggregate_level(const Bsr& A, double beta, int bs, int nvec, bool dr
     void* args[] = {(void*)&a0, (void*)&a1, (void*)&n, (void*)&a3, (void*)&a4, (void*)&a5};
     PhaseLog lg(s);
     lg.mark("  strength graph (nnz)", snnz);
-    TMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis2, blocks, TPB, args, 0, s));
+    TMG_CUDA(cudaLaunchCooperativeKernel(kfun, blocks, TPB, args, 0, s));
     note_launch();
     if (lg.on) lg.mark("  LFMIS (max sweeps)", read_int(rounds.get(), s));
   }
