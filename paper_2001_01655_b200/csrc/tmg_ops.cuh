@@ -98,6 +98,14 @@ __device__ __forceinline__ int fine_of_coarse(int I, int co, int nf, int idx[3],
   if (base + 1 < nf) { idx[c] = base + 1; w[c] = 0.5; ++c; }
   return c;
 }
+// the same as three fixed slots: valid candidates first, in order, then
+// (clamped index, weight 0) fillers
+__device__ __forceinline__ void fine_of_coarse3(int I, int co, int nf, int idx[3], double w[3]) {
+  const int c = fine_of_coarse(I, co, nf, idx, w);
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    if (q >= c) { idx[q] = idx[0]; w[q] = 0.0; }
+}
 // coarse parents of fine index i on one axis: up to 2 (index, weight)
 __device__ __forceinline__ int coarse_of_fine(int i, int co, int idx[2], double w[2]) {
   if (!co) { idx[0] = i; w[0] = 1.0; return 1; }
@@ -856,19 +864,25 @@ __global__ void __launch_bounds__(TPB, 1) k_restrict(Coarsening T, const double*
   const int K = blockIdx.z * blockDim.z + threadIdx.z;
   if (!(I < T.C.nn[0] && J < T.C.nn[1] && K < T.C.nn[2])) return;
   const int node = T.C.id(I, J, K);
+  // fixed 3^DIM gather (invalid candidates clamped, weight 0): every load is
+  // issued at once instead of one data-dependent loop trip at a time; the
+  // valid terms are summed in the same order, and the zero-weight ones add
+  // exact zeros, so the result is bit-identical
   int ix[3], iy[3], iz[3];
   double wx[3], wy[3], wz[3];
-  const int nx = fine_of_coarse(I, T.co[0], T.F.nn[0], ix, wx);
-  const int ny = fine_of_coarse(J, T.co[1], T.F.nn[1], iy, wy);
-  int nz = 1;
-  if (DIM == 3) nz = fine_of_coarse(K, T.co[2], T.F.nn[2], iz, wz);
-  else { iz[0] = 0; wz[0] = 1.0; }
+  fine_of_coarse3(I, T.co[0], T.F.nn[0], ix, wx);
+  fine_of_coarse3(J, T.co[1], T.F.nn[1], iy, wy);
+  if (DIM == 3) fine_of_coarse3(K, T.co[2], T.F.nn[2], iz, wz);
+  else { iz[0] = iz[1] = iz[2] = 0; wz[0] = 1.0; wz[1] = wz[2] = 0.0; }
   double acc[DIM];
 #pragma unroll
   for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
-  for (int c2 = 0; c2 < nz; ++c2)
-    for (int b = 0; b < ny; ++b)
-      for (int a = 0; a < nx; ++a) {
+#pragma unroll
+  for (int c2 = 0; c2 < (DIM == 3 ? 3 : 1); ++c2)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
         const double ww = wx[a] * wy[b] * wz[c2];
         double v[DIM];
         load_node<DIM>(r, T.F.id(ix[a], iy[b], iz[c2]), v);
