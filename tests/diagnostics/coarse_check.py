@@ -6,7 +6,7 @@ import sys
 import numpy as np
 import scipy.sparse.linalg as spla
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 from oracle import topomg_oracle as O  # noqa: E402
 from paper_2001_01655_b200 import problems as P  # noqa: E402

@@ -1,5 +1,5 @@
 import sys, numpy as np, scipy.sparse as sp
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+import os; _R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, 'tests'))
 from oracle import topomg_oracle as O
 import paper_2001_01655_b200 as T
 from test_gpu_parity import cantilever

@@ -100,7 +100,7 @@ def test_amg_pcg_matches_oracle(dims, beta, isolated):
 # 6-dof nodes whose candidate block [R_a; R_b] is rank deficient (exact zeros on
 # R's diagonal from the 2-node aggregates above), so the trailing Householder
 # columns of T are rounding noise in ANY implementation -- the reference is not
-# reproducible there either (tools/debug_hybrid.py shows the level-by-level split).
+# reproducible there either (tests/diagnostics/debug_hybrid.py shows the level-by-level split).
 @pytest.mark.parametrize("dims,n_geo,kind", [((16, 8, 8), 1, "weighted_jacobi"), ((16, 8, 8), 1, "chebyshev"),
                                              ((32, 16), 2, "weighted_jacobi"), ((24, 12, 12), 2, "chebyshev")])
 def test_hybrid_matches_oracle(dims, n_geo, kind):

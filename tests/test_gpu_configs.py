@@ -184,7 +184,7 @@ def test_full_size_config1_pcg_trajectories_match_oracle():
     DESIGN.md deviation 7).  The early agreement is limited by the coarsest
     operators (GMG: 2562 dofs, cond 4.6e13), whose direct solves differ in
     forward error at the percent level between any two implementations
-    (device explicit inverse vs scipy splu, tools/coarse_check.py)."""
+    (device explicit inverse vs scipy splu, tests/diagnostics/coarse_check.py)."""
     import os
     ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "config1_history.npz"))
     w, E = workload(1)
