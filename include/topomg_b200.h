@@ -158,6 +158,14 @@ int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_in
 /* multigrid.py:231 MgHierarchy.vcycle(b, k) (zero initial guess). */
 int tmg_hierarchy_vcycle(tmg_hierarchy* h, int32_t level, const double* b_dev, double* x_dev,
                          void* stream);
+/* multigrid.py:179 make_smoother(config, K): the finest level's smoother alone
+ * (no coarse levels; tmg_hierarchy_vcycle / the solvers reject it). */
+int tmg_smoother_create(tmg_operator* K, const tmg_smoother_desc* smoother, void* stream,
+                        tmg_hierarchy** out);
+/* The smoother's apply(x, b, passes) on a level (multigrid.py:57/90/131/161):
+ * x_dev in/out; levels below the coarsest of a V-cycle hierarchy. */
+int tmg_hierarchy_smooth(tmg_hierarchy* h, int32_t level, const double* b_dev, double* x_dev,
+                         int32_t passes, void* stream);
 /* y = A^level x (the Galerkin operator of a level), for parity checks. */
 int tmg_hierarchy_level_apply(tmg_hierarchy* h, int32_t level, const double* x_dev,
                               double* y_dev, void* stream);

@@ -13,7 +13,7 @@ from .material import SimpLaw
 from .mesh import (BoundaryConditions, StiffnessOperator, StructuredMesh, assemble_stiffness,
                    build_mesh, element_stiffness, rigid_body_modes)
 from .multigrid import (AdaptiveHybridController, MgHierarchy, SmootherConfig, adapt_after_solve, build_gmg,
-                        build_hybrid, build_sa_amg, gmg_level_dims)
+                        build_hybrid, build_sa_amg, gmg_level_dims, make_smoother, smooth)
 from .optimization import SolverHarness, compliance_and_sensitivity, element_strain_energies
 
 __version__ = "0.1.0"
@@ -22,6 +22,6 @@ __all__ = [
     "SolveConfig", "SolveRecord", "cg_solve", "pcg_solve", "solve", "gmres_solve", "fgmres_solve", "SimpLaw", "BoundaryConditions",
     "StiffnessOperator", "StructuredMesh", "assemble_stiffness", "build_mesh", "element_stiffness",
     "rigid_body_modes", "MgHierarchy", "SmootherConfig", "build_gmg", "build_hybrid", "build_sa_amg",
-    "gmg_level_dims", "AdaptiveHybridController", "adapt_after_solve",
+    "gmg_level_dims", "make_smoother", "smooth", "AdaptiveHybridController", "adapt_after_solve",
     "SolverHarness", "compliance_and_sensitivity", "element_strain_energies",
 ]

@@ -83,6 +83,8 @@ _SIGS = {
     "tmg_hierarchy_time_smoother": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _P]),
     "tmg_hierarchy_time_vcycle": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _P]),
     "tmg_hierarchy_time_phase": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _D, _P]),
+    "tmg_smoother_create": (C.c_int, [_P, _P, _P, _P]),
+    "tmg_hierarchy_smooth": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int32, _P]),
     "tmg_pcg_solve": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(SolveDesc), _P,
                                 C.POINTER(SolveRec), _P]),
     "tmg_gmres_solve": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(GmresDesc), _P,

@@ -468,9 +468,37 @@ int tmg_hierarchy_export(tmg_hierarchy* h, int32_t level, int32_t what, int64_t*
 int tmg_hierarchy_vcycle(tmg_hierarchy* h, int32_t level, const double* b, double* x, void* stream) {
   ABI_BEGIN
   TMG_REQUIRE(h, "hierarchy is NULL");
+  TMG_REQUIRE(!h->h->smoother_only, "a smoother-only hierarchy has no V-cycle");
   if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
   if (h->h->dim == 2) vcycle<2>(*h->h, level, b, x, S(stream));
   else vcycle<3>(*h->h, level, b, x, S(stream));
+  TMG_CUDA(cudaGetLastError());
+  ABI_END
+}
+
+int tmg_smoother_create(tmg_operator* K, const tmg_smoother_desc* smoother, void* stream, tmg_hierarchy** out) {
+  ABI_BEGIN
+  TMG_REQUIRE(K && out, "operator/out is NULL");
+  cudaStream_t s = S(stream);
+  DevBuf<double> ps;
+  const SmootherCfg c = to_cfg(smoother, K->op.ndof, ps, s);
+  auto H = std::make_unique<tmg_hierarchy>();
+  H->K = K;
+  if (K->op.dim == 2) H->h = build_smoother<2>(K->op, c, s);
+  else H->h = build_smoother<3>(K->op, c, s);
+  *out = H.release();
+  ABI_END
+}
+
+int tmg_hierarchy_smooth(tmg_hierarchy* h, int32_t level, const double* b, double* x, int32_t passes,
+                         void* stream) {
+  ABI_BEGIN
+  TMG_REQUIRE(h, "hierarchy is NULL");
+  TMG_REQUIRE(passes >= 0, "passes must be >= 0");
+  if (level < 0 || level >= (int)h->h->lv.size()) throw Error(TMG_ERANGE, "level index out of range");
+  if (level == h->h->last() && !h->h->smoother_only) throw Error(TMG_ERANGE, "the coarsest level has no smoother");
+  if (h->h->dim == 2) level_smooth<2>(*h->h, *h->h->lv[level], b, x, passes, S(stream));
+  else level_smooth<3>(*h->h, *h->h->lv[level], b, x, passes, S(stream));
   TMG_CUDA(cudaGetLastError());
   ABI_END
 }
@@ -603,6 +631,7 @@ int tmg_gmres_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* 
                     const tmg_gmres_desc* cfg, double* hist, tmg_solve_record* rec, void* stream) {
   ABI_BEGIN
   TMG_REQUIRE(K && cfg, "operator/config is NULL");
+  TMG_REQUIRE(!h || !h->h->smoother_only, "a smoother-only hierarchy cannot precondition (no V-cycle)");
   Hierarchy* H = h ? h->h.get() : nullptr;
   if (h) TMG_REQUIRE(h->h->lv[0]->op == &K->op, "hierarchy was built for a different operator");
   GmresResult r = K->op.dim == 2
@@ -625,6 +654,7 @@ int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x,
                   const tmg_solve_desc* cfg, double* hist, tmg_solve_record* rec, void* stream) {
   ABI_BEGIN
   TMG_REQUIRE(K && cfg, "operator/config is NULL");
+  TMG_REQUIRE(!h || !h->h->smoother_only, "a smoother-only hierarchy cannot precondition (no V-cycle)");
   Hierarchy* H = h ? h->h.get() : nullptr;
   if (h) TMG_REQUIRE(h->h->lv[0]->op == &K->op, "hierarchy was built for a different operator");
   std::unique_ptr<PcgCtx>& slot = h ? h->pcg : K->pcg;

@@ -64,6 +64,7 @@ struct Hierarchy {
   std::vector<int> provenance;  // 0 geometric, 1 algebraic (per level)
   std::vector<std::string> flags;
   bool drop_isolated = false;  // SA: leave strength-isolated nodes unaggregated (extension)
+  bool smoother_only = false;  // build_smoother: level 0 and its smoother, nothing else
   RedSlot red;                 // scratch reduction for setup
   int last() const { return (int)lv.size() - 1; }
   // fused-kernel V-cycle applies (point Jacobi, at least one pre-sweep)
@@ -581,6 +582,27 @@ std::unique_ptr<Hierarchy> build_gmg(const Operator& K, long long coarse_max_dof
   return H;
 }
 
+// make_smoother(config, K) (multigrid.py:179): a one-level "hierarchy" that
+// only carries the finest level's smoother (no coarse operator, no V-cycle)
+template <int DIM>
+std::unique_ptr<Hierarchy> build_smoother(const Operator& K, const SmootherCfg& sm, cudaStream_t s) {
+  auto H = new_hierarchy<DIM>(sm, 0, 0, s);
+  DevBuf<unsigned> bad;
+  bad.alloc(1, s);
+  bad.zero(s);
+  H->lv.push_back(fine_level<DIM>(K));
+  H->provenance.push_back(0);
+  level_setup<DIM>(*H, *H->lv[0], true, s, bad);
+  unsigned hbad = 0;
+  TMG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  TMG_CUDA(cudaStreamSynchronize(s));
+  if ((hbad & 5u) && sor_kind(sm.kind)) throw Error(-1, "zero diagonal; SOR sweep undefined");
+  if (hbad & 1u) throw Error(-1, "zero diagonal entry; operator not smoothable");
+  if ((hbad & 2u) && sm.kind == SM_BLOCK_JACOBI) throw Error(-1, "singular nodal block in block Jacobi smoother");
+  H->smoother_only = true;
+  return H;
+}
+
 // ----------------------------------------------------------------------------
 // V-cycle (multigrid.py:231), enqueue only
 // ----------------------------------------------------------------------------
@@ -729,6 +751,28 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
   }
   if (xcur != xout) TMG_CUDA(cudaMemcpyAsync(xout, xcur, l.ndof * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return dot_done;
+}
+
+// `passes` passes of the configured smoother on level l, x in/out (the
+// smoother classes' apply(x, b, passes), multigrid.py:57/90/131/161)
+template <int DIM>
+void level_smooth(Hierarchy& H, Level& l, const double* b, double* x, int passes, cudaStream_t s) {
+  if (passes <= 0) return;
+  const int kind = H.sm.kind;
+  if (cheb_kind(kind)) {
+    smooth_cheb<DIM>(H, l, b, x, false, passes, s);
+  } else if (kind == SM_SOR_GMRES) {
+    smooth_sor_gmres<DIM>(H, l, b, x, false, passes, s);
+  } else {
+    const Red nored{nullptr, nullptr, nullptr};
+    double* cur = x;
+    double* other = l.xt.get();
+    for (int p = 0; p < passes; ++p) {
+      lvl_sweep<DIM, false>(H, l, b, cur, other, nored, s);
+      std::swap(cur, other);
+    }
+    if (cur != x) TMG_CUDA(cudaMemcpyAsync(x, cur, l.ndof * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
 }
 
 }  // namespace tmg

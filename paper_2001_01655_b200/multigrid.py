@@ -128,6 +128,14 @@ class MgHierarchy:
 
     __call__ = apply
 
+    def smooth(self, x, b, passes=1, k=0, stream=None):
+        """`passes` passes of the level-k smoother on x (in place on a device
+        copy, returned): the smoother's apply(x, b, passes) (multigrid.py:57)."""
+        b = as_dev(b)
+        x = as_dev(x).clone()
+        _lib.check(_lib.load().tmg_hierarchy_smooth(self._h, int(k), ptr(b), ptr(x), int(passes), stream_ptr(stream)))
+        return x
+
     def level_apply(self, k, x):
         x = as_dev(x)
         out = empty_dev(x.numel())
@@ -233,6 +241,40 @@ def build_gmg(mesh, K, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, max_le
                                          C.byref(smoother.desc(K.shape[0])), int(n_pre), int(n_post),
                                          stream_ptr(stream), C.byref(h)))
     return MgHierarchy(h, K, smoother, n_pre, n_post, flags)
+
+
+class DeviceSmoother(MgHierarchy):
+    """make_smoother(config, A) of multigrid.py:179 for the stiffness operator:
+    the finest level's smoother on the device, ``apply(x, b, passes)`` like the
+    reference's smoother classes; ``lmax_estimate`` for the Chebyshev kinds."""
+
+    def apply(self, x, b, passes=1, stream=None):  # noqa: D401 - reference signature
+        return self.smooth(x, b, passes, 0, stream)
+
+    __call__ = apply
+
+    @property
+    def lmax_estimate(self):
+        return self.level_lmax(0)
+
+
+def make_smoother(config, K, block_size=None, stream=None):
+    """multigrid.py:179 on the device; K is the StiffnessOperator.  block_jacobi
+    uses nodal blocks (block_size = dofs per node)."""
+    if config.kind not in SMOOTHER_KINDS:
+        raise ValueError("unknown smoother kind %r" % config.kind)
+    dpn = K.mesh.dofs_per_node
+    if config.kind == "block_jacobi" and (block_size or config.block_size) != dpn:
+        raise ValueError("block_jacobi on the device uses nodal blocks of %d dofs" % dpn)
+    h = C.c_void_p()
+    _lib.check(_lib.load().tmg_smoother_create(K.handle, C.byref(config.desc(K.shape[0])), stream_ptr(stream),
+                                               C.byref(h)))
+    return DeviceSmoother(h, K, config, 0, 0)
+
+
+def smooth(config, K, x, b, passes=1):
+    """multigrid.py:190: `passes` smoothing passes of the configured kind on K x = b."""
+    return make_smoother(config, K).apply(x, b, passes)
 
 
 def _start_vector(n, seed):

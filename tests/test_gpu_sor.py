@@ -98,3 +98,37 @@ def test_sor_vcycle_is_deterministic():
     b = torch.as_tensor(np.random.default_rng(3).standard_normal(g.n_dofs), device="cuda")
     a1, a2 = host(h.apply(b)), host(h.apply(b))
     assert np.array_equal(a1, a2)
+
+
+@pytest.mark.parametrize("kind", ["sor_chebyshev", "sor_gmres"])
+def test_standalone_sor_smooth_matches_reference_golden(golden, kind):
+    """multigrid.smooth(SmootherConfig(kind, inner_iterations=3), K, 0, b, passes=2)
+    as the reference ran it in make_golden.py."""
+    mesh, bc, g, fixed, f, E, K, Kref = _device_problem((16, 8), 2)
+    x = T.smooth(T.SmootherConfig(kind=kind, inner_iterations=3), K, np.zeros(K.shape[0]), golden["sor2d_b"], passes=2)
+    assert rel(host(x), golden["sor2d_%s_smooth" % kind]) <= 1e-9
+
+
+@pytest.mark.parametrize("dims,kind", [((24, 12), "weighted_jacobi"), ((24, 12), "block_jacobi"),
+                                       ((24, 12), "chebyshev"), ((24, 12), "sor_chebyshev"),
+                                       ((24, 12), "sor_gmres"), ((6, 4, 4), "weighted_jacobi"),
+                                       ((6, 4, 4), "block_jacobi"), ((6, 4, 4), "sor_chebyshev"),
+                                       ((6, 4, 4), "sor_gmres")])
+def test_standalone_smoothers_match_oracle(dims, kind):
+    """make_smoother(config, K).apply(x, b, passes) (multigrid.py:179) from a
+    nonzero start, against the oracle's smoother classes."""
+    mesh, g, bc, rho, E, K, Kref = cantilever(dims, 4)
+    w = 1.0 if kind == "chebyshev" else 0.6
+    sm = T.make_smoother(T.SmootherConfig(kind=kind, weight=w, inner_iterations=2, block_size=len(dims)), K)
+    so = O.make_smoother(O.Smoother(kind, w, inner_iterations=2, block_size=len(dims)), Kref)
+    rng = np.random.default_rng(8)
+    x0 = rng.standard_normal(g.n_dofs)
+    x0[bc.fixed_dofs] = 0.0
+    b = rng.standard_normal(g.n_dofs)
+    x = host(sm.apply(x0, b, 3))
+    xo = so.apply(x0.copy(), b, 3)
+    assert rel(x, xo) <= 1e-9, kind
+    if kind in ("chebyshev", "sor_chebyshev"):
+        assert abs(sm.lmax_estimate - so.lmax_estimate) <= 1e-10 * so.lmax_estimate
+    with pytest.raises(ValueError):  # a smoother is not a preconditioner
+        sm.vcycle(b)
