@@ -176,9 +176,11 @@ template <int DIM>
 void lvl_cheb_step(const Level& l, const double* rin, const double* zs, const double* dv, const double* pin, int i,
                    bool x_zero, double* x, double* po, double* ro, cudaStream_t s) {
   if (l.lattice()) {
+    // ro == nullptr marks the last step of a pass: neither r' nor p' is read
+    // again (lattice rows form p' of their neighbours on the fly)
     with_lattice<DIM>(l, [&](auto o) {
       launch(k_cheb<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, rin, zs, pin, dv, l.coef.get(), i, x_zero ? 1 : 0, x,
-                                                           po, ro);
+                                                           ro ? po : nullptr, ro);
     });
     note_launch();
   } else {

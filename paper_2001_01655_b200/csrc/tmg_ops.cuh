@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
         xv[c] += alpha * pv[c];
         rr[c] -= alpha * o[c];
       }
-      store_node<DIM>(po, node, pv);
+      if (po) store_node<DIM>(po, node, pv);
       store_node<DIM>(x, node, xv);
       if (ro) store_node<DIM>(ro, node, rr);
     });
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
     xv[c] += alpha * pv[c];
     rr[c] -= alpha * out[c];
   }
-  store_node<DIM>(po, node, pv);
+  if (po) store_node<DIM>(po, node, pv);  // nullptr: last step of a pass, p' is never read
   store_node<DIM>(x, node, xv);
   if (ro) store_node<DIM>(ro, node, rr);  // nullptr: last step of a pass, r' is never read
 }
