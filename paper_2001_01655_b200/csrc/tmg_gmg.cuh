@@ -735,10 +735,10 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
       if (p == 0 && fuse_prolong) {
         with_lattice<DIM>(l, [&](auto o) {
           if (last)
-            launch(k_prolong_jacobi<DIM, decltype(o), true>, TMG_NODE_LAUNCH(l), s, 
+            launch(k_prolong_jacobi<DIM, decltype(o), true>, TMG_ROW_OP_LAUNCH(l), s, 
                 o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, *dot);
           else
-            launch(k_prolong_jacobi<DIM, decltype(o), false>, TMG_NODE_LAUNCH(l), s, 
+            launch(k_prolong_jacobi<DIM, decltype(o), false>, TMG_ROW_OP_LAUNCH(l), s, 
                 o, xcur, c.x.get(), l.T, b, l.dinv.get(), l.wdev.get(), dst, nored);
         });
         note_launch();

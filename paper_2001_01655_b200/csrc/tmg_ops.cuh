@@ -236,7 +236,16 @@ struct FineOp {
   // one-node halo: the source vector (unmasked), the free-dof masks and the
   // moduli of the (BX+1)(BY+1)(BZ+1) elements touching the tile.  Every value is
   // read from L2/HBM once per block instead of once per neighbouring thread.
-  static constexpr int BX = 32, BY = DIM == 2 ? 8 : 4, BZ = DIM == 2 ? 1 : 2;
+#ifndef TMG_F3_BX
+#define TMG_F3_BX 16
+#define TMG_F3_BY 4
+#define TMG_F3_BZ 4
+#endif
+  // 3D tile 16x4x4 (648 staged nodes / 425 elements per 256 rows; 32x4x2: 816 /
+  // 495).  Measured config-4 sweep / residual: 16x4x4 145 / 103 us, 16x8x2 151 /
+  // 106, 32x2x4 157 / 110, 32x4x2 157 / 111, 8x8x4 173 / 125.
+  static constexpr int BX = DIM == 2 ? 32 : TMG_F3_BX, BY = DIM == 2 ? 8 : TMG_F3_BY, BZ = DIM == 2 ? 1 : TMG_F3_BZ;
+  static_assert(BX * BY * BZ == TPB, "FineOp tile must have TPB threads");
   static constexpr int HX = BX + 2, HY = BY + 2, HZ = DIM == 2 ? 1 : BZ + 2;
   static constexpr int EX = BX + 1, EY = BY + 1, EZ = DIM == 2 ? 1 : BZ + 1;
   static constexpr int NH = HX * HY * HZ, NEL = EX * EY * EZ;
@@ -490,6 +499,7 @@ struct StencilOp {
   // batch before any arithmetic) so a thread has G*(DD+DIM) loads in flight --
   // coarse levels have too few threads to hide L2 latency by occupancy alone.
   static constexpr size_t SMEM_BYTES = 0;
+  static constexpr int BX = 32, BY = DIM == 2 ? 8 : 4, BZ = DIM == 2 ? 1 : 2;  // = node_block<DIM>()
 #ifndef TMG_ST_MINB
 #define TMG_ST_MINB 2  // 3D stencil rows: 128 instead of 254 registers (config-3 PCG 370.8 -> 355.7 us/iter; 3 / 4: slower)
 #endif
@@ -548,12 +558,12 @@ struct StencilOp {
 template <int DIM, class Op>
 inline dim3 row_grid(const Lat& L) {
   if constexpr (Op::STREAM) return f3::grid(L);
-  else return node_grid<DIM>(L);
+  else return dim3((L.nn[0] + Op::BX - 1) / Op::BX, (L.nn[1] + Op::BY - 1) / Op::BY, (L.nn[2] + Op::BZ - 1) / Op::BZ);
 }
 template <int DIM, class Op>
 inline dim3 row_block() {
   if constexpr (Op::STREAM) return dim3(f3::NT, 1, 1);
-  else return node_block<DIM>();
+  else return dim3(Op::BX, Op::BY, Op::BZ);
 }
 template <class Op>
 constexpr size_t row_smem() {
