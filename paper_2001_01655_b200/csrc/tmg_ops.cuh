@@ -244,7 +244,12 @@ struct FineOp {
   // 3D tile 16x4x4 (648 staged nodes / 425 elements per 256 rows; 32x4x2: 816 /
   // 495).  Measured config-4 sweep / residual: 16x4x4 145 / 103 us, 16x8x2 151 /
   // 106, 32x2x4 157 / 110, 32x4x2 157 / 111, 8x8x4 173 / 125.
-  static constexpr int BX = DIM == 2 ? 32 : TMG_F3_BX, BY = DIM == 2 ? 8 : TMG_F3_BY, BZ = DIM == 2 ? 1 : TMG_F3_BZ;
+#ifndef TMG_F2_BX
+#define TMG_F2_BX 32
+#define TMG_F2_BY 8
+#endif
+  static constexpr int BX = DIM == 2 ? TMG_F2_BX : TMG_F3_BX, BY = DIM == 2 ? TMG_F2_BY : TMG_F3_BY,
+                       BZ = DIM == 2 ? 1 : TMG_F3_BZ;
   static_assert(BX * BY * BZ == TPB, "FineOp tile must have TPB threads");
   static constexpr int HX = BX + 2, HY = BY + 2, HZ = DIM == 2 ? 1 : BZ + 2;
   static constexpr int EX = BX + 1, EY = BY + 1, EZ = DIM == 2 ? 1 : BZ + 1;
