@@ -381,7 +381,7 @@ int tmg_hierarchy_level_info(const tmg_hierarchy* h, int32_t level, tmg_level_in
     info->nonzeros = l.op->nelem;
   } else if (l.opkind == OP_STENCIL) {
     info->storage = 1;
-    info->nonzeros = (D == 2 ? 9 : 27) * (long long)D * D * l.L.n;
+    info->nonzeros = (D == 2 ? StencilOp<2>::NH : StencilOp<3>::NH) * (long long)D * D * l.L.n;  // symmetric: upper slots
   } else {
     info->storage = 2;
     info->nonzeros = l.Ab.scalar_nnz();

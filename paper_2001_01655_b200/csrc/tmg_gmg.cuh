@@ -550,9 +550,9 @@ void add_geometric_levels(Hierarchy& H, const std::vector<std::array<int, 3>>& p
     f.T = T;
     f.xfer = XF_GEO;
     H.provenance.back() = 0;
-    l->A.alloc((size_t)Slots<DIM>::NS * DIM * DIM * l->L.n, s);
+    l->A.alloc((size_t)StencilOp<DIM>::NH * DIM * DIM * l->L.n, s);
     with_lattice<DIM>(f, [&](auto o) {
-      const long long nt = l->L.n * Slots<DIM>::NS;
+      const long long nt = l->L.n * StencilOp<DIM>::NH;
       launch(k_rap<DIM, decltype(o)>, grid_for(nt), TPB, 0, s, o, T, l->A.get());
       note_launch();
     });

@@ -496,9 +496,37 @@ namespace tmg {
 // ----------------------------------------------------------------------------
 template <int DIM>
 struct StencilOp {
-  static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
+  // 2D: a Galerkin operator is symmetric, so only the centre and the "upper"
+  // slots (s >= C0, offsets lexicographically >= 0) are stored, A[(h*DD + q)*n +
+  // node] with h = s - C0; a lower slot of node i is the transposed upper block of
+  // its neighbour, read at the neighbour's index (unit-stride across a warp):
+  // 5 of 9 blocks per node (config-1 GMG PCG iteration -2.5 %).  3D keeps all 27
+  // slots (C0 = 0): the mirrored loads of 13 slots push the batched, fully
+  // unrolled row past its register budget (measured 84 -> 98-216 us per config-4
+  // level-1 sweep in every variant tried).
+  static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM, C0 = DIM == 2 ? NS / 2 : 0, NH = NS - C0;
   Lat L;
   const double* __restrict__ A;
+  // block of slot s at node (i, j, k) into av; a lower slot whose neighbour is
+  // outside the lattice reads the node's own (finite) storage: the caller zeroes
+  // the block (block()) or the neighbour's value (row()) then
+  __device__ __forceinline__ bool slot_block(int s, int node, int i, int j, int k, double av[DD]) const {
+    const int n = (int)L.n;
+    if (s >= C0) {
+#pragma unroll
+      for (int q = 0; q < DD; ++q) av[q] = ldv(A + ((s - C0) * DD + q) * n + node);
+      return true;
+    }
+    const int ii = i + Slots<DIM>::dx(s), jj = j + Slots<DIM>::dy(s), kk = k + Slots<DIM>::dz(s);
+    const bool in = L.inside(ii, jj, DIM == 3 ? kk : 0);
+    const int nb = in ? L.id(ii, jj, DIM == 3 ? kk : 0) : node;
+    const int h = (NS - 1 - s) - C0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) av[a * DIM + b] = ldv(A + (h * DD + b * DIM + a) * n + nb);
+    return in;
+  }
 
   // Loads are issued in batches of G slots (all coefficient and vector loads of a
   // batch before any arithmetic) so a thread has G*(DD+DIM) loads in flight --
@@ -528,9 +556,11 @@ struct StencilOp {
         const int ii = min(max(i + Slots<DIM>::dx(s), 0), L.nn[0] - 1);
         const int jj = min(max(j + Slots<DIM>::dy(s), 0), L.nn[1] - 1);
         const int kk = DIM == 3 ? min(max(k + Slots<DIM>::dz(s), 0), L.nn[2] - 1) : 0;
-        src.load(L.id(ii, jj, kk), ii, jj, kk, xv[g]);  // clamped; the slot's coefficients are 0 there
+        src.load(L.id(ii, jj, kk), ii, jj, kk, xv[g]);  // clamped; upper-slot coefficients are 0 there
+        if (!slot_block(s, node, i, j, k, av[g])) {      // lower slot off the lattice: no contribution
 #pragma unroll
-        for (int q = 0; q < DD; ++q) av[g][q] = ldv(A + (s * DD + q) * n + node);
+          for (int d = 0; d < DIM; ++d) xv[g][d] = 0.0;
+        }
       }
       reg_fence<G * DIM>(&xv[0][0]);
       reg_fence<G * DD>(&av[0][0]);
@@ -552,9 +582,9 @@ struct StencilOp {
 
   __device__ void block(int i0, int i1, int i2, int j0, int j1, int j2, double blk[DD]) const {
     const int s = Slots<DIM>::of(j0 - i0, j1 - i1, DIM == 3 ? j2 - i2 : 0);
-    const int node = L.id(i0, i1, i2);
+    if (!slot_block(s, L.id(i0, i1, i2), i0, i1, i2, blk))
 #pragma unroll
-    for (int t = 0; t < DD; ++t) blk[t] = A[(s * DD + t) * L.n + node];
+      for (int t = 0; t < DD; ++t) blk[t] = 0.0;
   }
 };
 
@@ -938,11 +968,11 @@ __global__ void __launch_bounds__(TPB, 1) k_prolong_add(Coarsening T, const doub
 template <int DIM, class Op>
 __global__ void __launch_bounds__(TPB, 1) k_rap(const __grid_constant__ Op op, Coarsening T, double* __restrict__ Ac) {
   TMG_PDL_ENTRY;
-  constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM;
+  constexpr int DD = DIM * DIM, C0 = StencilOp<DIM>::C0, NH = StencilOp<DIM>::NH;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= T.C.n * NS) return;
-  const int s = (int)(t / T.C.n);
-  const long long node = t - (long long)s * T.C.n;
+  if (t >= T.C.n * NH) return;  // the stored slots of StencilOp
+  const int s = C0 + (int)(t / T.C.n);
+  const long long node = t - (long long)(s - C0) * T.C.n;
   int I0, I1, I2;
   T.C.ijk(node, I0, I1, I2);
   const int J0 = I0 + Slots<DIM>::dx(s), J1 = I1 + Slots<DIM>::dy(s), J2 = I2 + Slots<DIM>::dz(s);
@@ -982,7 +1012,7 @@ __global__ void __launch_bounds__(TPB, 1) k_rap(const __grid_constant__ Op op, C
         }
   }
 #pragma unroll
-  for (int q = 0; q < DD; ++q) Ac[(s * DD + q) * T.C.n + node] = acc[q];
+  for (int q = 0; q < DD; ++q) Ac[((s - C0) * DD + q) * T.C.n + node] = acc[q];
 }
 
 }  // namespace tmg
