@@ -504,7 +504,11 @@ struct StencilOp {
   // slots (C0 = 0): the mirrored loads of 13 slots push the batched, fully
   // unrolled row past its register budget (measured 84 -> 98-216 us per config-4
   // level-1 sweep in every variant tried).
-  static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM, C0 = DIM == 2 ? NS / 2 : 0, NH = NS - C0;
+#ifndef TMG_ST_SYM3
+#define TMG_ST_SYM3 0
+#endif
+  static constexpr int NS = Slots<DIM>::NS, DD = DIM * DIM, C0 = (DIM == 2 || TMG_ST_SYM3) ? NS / 2 : 0,
+                       NH = NS - C0;
   Lat L;
   const double* __restrict__ A;
   // block of slot s at node (i, j, k) into av; a lower slot whose neighbour is
