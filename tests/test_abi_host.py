@@ -116,3 +116,32 @@ def test_solve_config_validation_and_methods():
     for bad in (dict(rtol=0.0), dict(rtol=1.0), dict(restart=0)):
         with pytest.raises(ValueError):
             SolveConfig(**bad)
+
+
+def test_smoother_descriptor_host_logic():
+    """SmootherConfig -> tmg_smoother_desc: every reference kind is known, the
+    sor_chebyshev descriptor carries multigrid.py:119's power-method start vector
+    (default_rng(0), the smoother is built with seed 0) for the finest level."""
+    from paper_2001_01655_b200 import SmootherConfig
+    from paper_2001_01655_b200.multigrid import SMOOTHER_KINDS
+    assert set(SMOOTHER_KINDS) >= {"weighted_jacobi", "block_jacobi", "sor_chebyshev", "sor_gmres"}
+    d = SmootherConfig(kind="sor_chebyshev", inner_iterations=3).desc(257)
+    assert d.kind == SMOOTHER_KINDS["sor_chebyshev"] and d.inner_iterations == 3
+    ps = np.ctypeslib.as_array((C.c_double * 257).from_address(d.power_start))
+    assert np.array_equal(ps, np.random.default_rng(0).standard_normal(257))
+    assert not SmootherConfig(kind="sor_gmres").desc(10).power_start
+    assert not SmootherConfig(kind="sor_gmres").stationary and SmootherConfig().stationary
+    with pytest.raises(ValueError):
+        SmootherConfig(kind="sor").desc(10)
+    with pytest.raises(ValueError):
+        SmootherConfig(weight=0.0)
+
+
+def test_solve_descriptor_defaults_to_cg():
+    """tmg_solve_desc zero-initialised fields keep the CG extension; method/restart
+    select krylov.solve's GMRES / FGMRES in the host-buffer entry."""
+    L = lib()
+    d = L.SolveDesc(1e-8, 100)
+    assert (d.method, d.restart) == (0, 0)
+    d = L.SolveDesc(1e-8, 100, 2, 7)
+    assert (d.method, d.restart) == (2, 7)
