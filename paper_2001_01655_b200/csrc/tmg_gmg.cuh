@@ -473,8 +473,13 @@ void coarse_setup(Hierarchy& H, cudaStream_t s) {
 inline void pad_cycle_operators(Hierarchy& H, cudaStream_t s) {
   const char* e = std::getenv("TMG_BSR_PAD");
   if (e && e[0] == '0') return;
-  for (auto& lp : H.lv)
+  for (auto& lp : H.lv) {
     if (!lp->lattice()) bsr_pad_blocks(lp->Ab, s);
+    if (lp->xfer == XF_SPARSE) {  // 3x3 transfers between algebraic levels
+      bsr_pad_blocks(lp->P, s);
+      bsr_pad_blocks(lp->Pt, s);
+    }
+  }
 }
 
 inline void finalize_checks(Hierarchy& H, DevBuf<unsigned>& bad, cudaStream_t s) {
