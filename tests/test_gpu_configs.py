@@ -237,3 +237,29 @@ def test_full_size_config2_solves_match_oracle():
         assert abs(rec.iterations - it_ref) <= 1
         assert abs(c - cr) <= 1e-9 * abs(cr)
         assert np.linalg.norm(W @ uh - pr) <= 1e-7 * np.linalg.norm(pr)
+
+
+def test_full_size_config3_trajectory_matches_oracle():
+    """BASELINE config 3 at full size (698,691 dofs, 3D GMG-4, Jacobi-Chebyshev
+    degree 2 with Lanczos bounds): the oracle's own first 200 PCG iterations
+    (tests/golden/make_config3_history.py) -- same level sizes, same Lanczos
+    bounds, the same residual trajectory."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "config3_history.npz")
+    if not os.path.exists(path):
+        pytest.skip("config3_history.npz not generated")
+    ref = np.load(path)
+    w, E = workload(3)
+    K = T.assemble_stiffness(w.mesh, w.bc, E)
+    h = LegRunner(w, w.solvers[0]).build(K)
+    assert [lv.size for lv in h.levels] == list(ref["sizes"])
+    lm = np.array([h.level_lmax(k) for k in range(h.n_levels - 1)])
+    u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=200))
+    hist, rh = np.array(rec.residual_history), ref["hist"]
+    d = np.abs(hist - rh) / rh
+    print("lmax rel", np.abs(lm - ref["lmax"]) / ref["lmax"], "trajectory rel diff at 10/50/100/200:",
+          [float(d[k]) for k in (10, 50, 100, 200)])
+    assert np.max(np.abs(lm - ref["lmax"]) / ref["lmax"]) <= 1e-10
+    assert len(hist) == len(rh) == 201
+    assert d[:51].max() <= 1e-6  # measured 1e-9 at 10, 1.3e-7 at 50, 2.3e-6 at 200
+    assert d.max() <= 1e-5
