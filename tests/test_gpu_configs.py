@@ -263,3 +263,39 @@ def test_full_size_config3_trajectory_matches_oracle():
     assert len(hist) == len(rh) == 201
     assert d[:51].max() <= 1e-6  # measured 1e-9 at 10, 1.3e-7 at 50, 2.3e-6 at 200
     assert d.max() <= 1e-5
+
+
+def test_full_size_config4_trajectory_matches_oracle():
+    """BASELINE config 4 at full size (5,447,811 dofs, hybrid: 3 geometric levels
+    then SA-AMG, Jacobi-Chebyshev everywhere): the oracle's own first 20 PCG
+    iterations (tests/golden/make_config4_history.py) -- same level sizes
+    (geometric and aggregated), same Lanczos bounds, same residual trajectory."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "config4_history.npz")
+    if not os.path.exists(path):
+        pytest.skip("config4_history.npz not generated")
+    ref = np.load(path)
+    w, E = workload(4)
+    K = T.assemble_stiffness(w.mesh, w.bc, E)
+    h = LegRunner(w, w.solvers[0]).build(K)
+    assert [lv.size for lv in h.levels] == list(ref["sizes"])
+    lm = np.array([h.level_lmax(k) for k in range(h.n_levels - 1)])
+    u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=20))
+    hist, rh = np.array(rec.residual_history), ref["hist"]
+    d = np.abs(hist - rh) / rh
+    print("lmax rel", np.abs(lm - ref["lmax"]) / ref["lmax"], "trajectory rel diff:", np.array2string(d, precision=2))
+    # The first SA level (407 aggregates on the 12,675-dof operator) has 36
+    # two-node aggregates: two 3-dof nodes carry a rank-5 block of the 6 rigid
+    # modes, so one Householder column of T per such aggregate is rounding noise
+    # in ANY implementation (reference included, DESIGN.md "Case excluded on
+    # purpose"); the operators below it, their Lanczos bound (8.6e-4) and from
+    # iteration 1 the trajectory (0.2-0.5 %, growing to 1-2 % by iteration 20)
+    # differ for that reason alone: the oracle against itself with the SA
+    # candidates perturbed by 1e-14 shows the same (deepest bound 1.2e-3,
+    # trajectory 1-2 %; diagnostics/config4_noise_drift.py).
+    rl = np.abs(lm - ref["lmax"]) / ref["lmax"]
+    assert rl[:4].max() <= 1e-12  # the geometric levels and the first SA level
+    assert len(hist) == len(rh) == 21
+    assert d[0] <= 1e-12                  # same load vector, same initial residual
+    assert d[:5].max() <= 1e-2
+    assert d.max() <= 5e-2
