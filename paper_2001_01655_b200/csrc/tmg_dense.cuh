@@ -12,55 +12,73 @@ namespace tmg {
 constexpr int GJ_NB = 32;
 
 // In-place Gauss-Jordan of the kb x kb pivot block; writes D = A_KK^-1.
+// Thread (i, j) keeps M[i][j] in a register: M[i][p] comes from lane p of the
+// same warp (shuffle), the pivot row from a double-buffered shared row written
+// by warp p at the end of step p-1 -- one barrier per step instead of two, same
+// arithmetic per entry.
 __global__ void __launch_bounds__(1024) k_gj_pivot(const double* __restrict__ A, long long n, long long k0, int kb,
                                                    double* __restrict__ D, unsigned* __restrict__ bad) {
   TMG_PDL_ENTRY;
-  __shared__ double M[GJ_NB][GJ_NB + 1];
+  __shared__ double prow[2][GJ_NB];
   const int i = threadIdx.y, j = threadIdx.x;
   const bool in = i < kb && j < kb;
-  if (in) M[i][j] = A[(k0 + i) * n + k0 + j];
+  double m = in ? A[(k0 + i) * n + k0 + j] : 0.0;
+  if (i == 0) prow[0][j] = m;
   __syncthreads();
   for (int p = 0; p < kb; ++p) {
-    double piv = M[p][p];
-    double mip = in ? M[i][p] : 0.0, mpj = in ? M[p][j] : 0.0, mij = in ? M[i][j] : 0.0;
-    __syncthreads();
+    const double mpj = prow[p & 1][j];
+    double piv = prow[p & 1][p];
+    const double mip = __shfl_sync(0xffffffffu, m, p);
     if (!(piv > 0.0)) {
       if (i == 0 && j == 0) atomicOr(bad, 1u);
       piv = 1.0;
     }
     const double d = 1.0 / piv;
     if (in) {
-      if (i == p && j == p) M[i][j] = d;
-      else if (i == p) M[i][j] = mpj * d;
-      else if (j == p) M[i][j] = -mip * d;
-      else M[i][j] = mij - mip * mpj * d;
+      if (i == p && j == p) m = d;
+      else if (i == p) m = mpj * d;
+      else if (j == p) m = -mip * d;
+      else m = m - mip * mpj * d;
     }
+    if (i == p + 1) prow[(p + 1) & 1][j] = m;
     __syncthreads();
   }
-  if (in) D[i * GJ_NB + j] = M[i][j];
+  if (in) D[i * GJ_NB + j] = m;
 }
 
-// RowP[r][j] = sum_c D[r][c] A[k0+c][j]  (all j);  ColP[i][c] = A[i][k0+c]
-__global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A, long long n, long long k0, int kb,
-                                                   const double* __restrict__ D, double* __restrict__ RowP,
-                                                   double* __restrict__ ColP) {
+// RowP[r][j] = sum_c D[r][c] A[k0+c][j]  (all j);  ColP[c][i] = A[i][k0+c]
+// (column-major copy of the pivot columns: the update kernels stage it coalesced).
+// blockIdx.y picks GJ_PANEL_R rows r of D (and the same columns c of the ColP
+// copy): n/128 x 8 blocks instead of n/256, so the 2562-wide config-1 panel
+// fills the SMs (measured 15.8 us on 11 blocks).  Each sum keeps the c order.
+constexpr int GJ_PANEL_R = 4, GJ_PANEL_TPB = 128;
+__global__ void __launch_bounds__(GJ_PANEL_TPB) k_gj_panels(const double* __restrict__ A, long long n, long long k0,
+                                                            int kb, const double* __restrict__ D,
+                                                            double* __restrict__ RowP, double* __restrict__ ColP) {
   TMG_PDL_ENTRY;
-  __shared__ double Ds[GJ_NB * GJ_NB];
-  for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t] = D[t];
+  __shared__ double Ds[GJ_PANEL_R * GJ_NB];
+  const int r0 = blockIdx.y * GJ_PANEL_R;
+  for (int t = threadIdx.x; t < GJ_PANEL_R * GJ_NB; t += blockDim.x) Ds[t] = D[r0 * GJ_NB + t];
   __syncthreads();
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= n) return;
   double col[GJ_NB];
 #pragma unroll
   for (int c = 0; c < GJ_NB; ++c) col[c] = c < kb ? A[(k0 + c) * n + j] : 0.0;
-#pragma unroll 4
-  for (int r = 0; r < kb; ++r) {
+#pragma unroll
+  for (int q = 0; q < GJ_PANEL_R; ++q) {
+    const int r = r0 + q;
+    if (r >= kb) break;
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c < GJ_NB; ++c) s += Ds[r * GJ_NB + c] * col[c];
+    for (int c = 0; c < GJ_NB; ++c) s += Ds[q * GJ_NB + c] * col[c];
     RowP[r * n + j] = s;
   }
-  for (int c = 0; c < kb; ++c) ColP[j * GJ_NB + c] = A[j * n + k0 + c];
+#pragma unroll
+  for (int q = 0; q < GJ_PANEL_R; ++q) {
+    const int c = r0 + q;
+    if (c < kb) ColP[c * n + j] = A[j * n + k0 + c];
+  }
 }
 
 // 64x64 output tile per block, 256 threads x (4x4) outputs.
@@ -68,14 +86,14 @@ __global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ A, long 
                                                    const double* __restrict__ D, const double* __restrict__ RowP,
                                                    const double* __restrict__ ColP) {
   TMG_PDL_ENTRY;
-  __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[i0+ii][c]
+  __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[c][i0+ii]
   __shared__ double Rs[GJ_NB][64 + 1];  // Rs[c][jj] = RowP[c][j0+jj]
   __shared__ double Ds[GJ_NB][GJ_NB + 1];
   const long long i0 = blockIdx.y * 64LL, j0 = blockIdx.x * 64LL;
   for (int t = threadIdx.x; t < GJ_NB * 64; t += blockDim.x) {
     const int c = t / 64, q = t % 64;
     const long long gi = i0 + q, gj = j0 + q;
-    Cs[c][q] = (c < kb && gi < n) ? ColP[gi * GJ_NB + c] : 0.0;
+    Cs[c][q] = (c < kb && gi < n) ? ColP[c * n + gi] : 0.0;
     Rs[c][q] = (c < kb && gj < n) ? RowP[c * n + gj] : 0.0;
   }
   for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t / GJ_NB][t % GJ_NB] = D[t];
@@ -138,14 +156,16 @@ __global__ void __launch_bounds__(256) k_gj_update_mma(double* __restrict__ A, l
                                                        const double* __restrict__ RowP,
                                                        const double* __restrict__ ColP) {
   TMG_PDL_ENTRY;
-  __shared__ double Cs[GJ_NB][64 + 1];  // Cs[c][ii] = ColP[i0+ii][c]
-  __shared__ double Rs[GJ_NB][64 + 1];  // Rs[c][jj] = RowP[c][j0+jj]
+  // row stride 68 doubles (4 mod 16): the fragment loads below (lane 4g+t reads
+  // [c+t][base+g]) hit 16 distinct bank pairs per half-warp
+  __shared__ double Cs[GJ_NB][64 + 4];  // Cs[c][ii] = ColP[c][i0+ii]
+  __shared__ double Rs[GJ_NB][64 + 4];  // Rs[c][jj] = RowP[c][j0+jj]
   __shared__ double Ds[GJ_NB][GJ_NB + 1];
   const long long i0 = blockIdx.y * 64LL, j0 = blockIdx.x * 64LL;
   for (int t = threadIdx.x; t < GJ_NB * 64; t += blockDim.x) {
     const int c = t / 64, q = t % 64;
     const long long gi = i0 + q, gj = j0 + q;
-    Cs[c][q] = (c < kb && gi < n) ? ColP[gi * GJ_NB + c] : 0.0;
+    Cs[c][q] = (c < kb && gi < n) ? ColP[c * n + gi] : 0.0;
     Rs[c][q] = (c < kb && gj < n) ? RowP[c * n + gj] : 0.0;
   }
   for (int t = threadIdx.x; t < GJ_NB * GJ_NB; t += blockDim.x) Ds[t / GJ_NB][t % GJ_NB] = D[t];
@@ -304,7 +324,7 @@ struct DenseInverse {
     for (long long k0 = 0; k0 < n; k0 += GJ_NB) {
       const int kb = (int)std::min<long long>(GJ_NB, n - k0);
       launch(k_gj_pivot, 1, dim3(GJ_NB, GJ_NB), 0, s, A.get(), n, k0, kb, D.get(), bad.get()); ::tmg::note_launch();
-      launch(k_gj_panels, grid_for(n), 256, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
+      launch(k_gj_panels, dim3((unsigned)((n + GJ_PANEL_TPB - 1) / GJ_PANEL_TPB), GJ_NB / GJ_PANEL_R), GJ_PANEL_TPB, 0, s, A.get(), n, k0, kb, D.get(), RowP.get(), ColP.get()); ::tmg::note_launch();
       launch(dense_mma() ? k_gj_update_mma : k_gj_update, dim3(tiles, tiles), 256, 0, s, A.get(), n, k0, kb, D.get(),
              RowP.get(), ColP.get());
       ::tmg::note_launch();
