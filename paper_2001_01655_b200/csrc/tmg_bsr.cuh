@@ -9,6 +9,16 @@
 
 #include "tmg_ops.cuh"
 
+#ifndef TMG_BSR_MINB
+#define TMG_BSR_MINB 4  // min CTAs per SM of the square BSR row kernels (64 registers; measured 1/4/6/8)
+#endif
+#ifndef TMG_BSR_XFER_MINB
+// min CTAs per SM of the transfer kernels (P, P^T): 6 for the 2D level-0 2x3 /
+// 3x2 blocks (config 2 AMG iteration 660 -> 642 us), 4 otherwise (the 3x3 and
+// the 3D 3x6 / 6x6 transfers are slower at 6)
+#define TMG_BSR_XFER_MINB ((R * C == 6) ? 6 : 4)
+#endif
+
 namespace tmg {
 
 struct Bsr {
@@ -129,7 +139,7 @@ __device__ __forceinline__ void bsr_row(const BsrView<R, C>& A, int row, int lan
 
 // y = A x (+ y if accumulate)
 template <int R, int C>
-__global__ void __launch_bounds__(TPB) k_bsr_apply(BsrView<R, C> A, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, TMG_BSR_XFER_MINB) k_bsr_apply(BsrView<R, C> A, const double* __restrict__ x,
                                                    double* __restrict__ y, int accumulate) {
   TMG_PDL_ENTRY;
   int lane;
@@ -147,7 +157,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_apply(BsrView<R, C> A, const double
 // bc = P^T r as a BSR product with the stored transpose; optional fused first
 // zero-start Jacobi sweep of the coarse level, xc = w dinvc .* bc
 template <int R, int C>
-__global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const double* __restrict__ r,
+__global__ void __launch_bounds__(TPB, TMG_BSR_XFER_MINB) k_bsr_restrict(BsrView<R, C> Pt, const double* __restrict__ r,
                                                       double* __restrict__ bc, const double* __restrict__ dinvc,
                                                       const double* __restrict__ wp, double* __restrict__ xc) {
   TMG_PDL_ENTRY;
@@ -167,7 +177,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_restrict(BsrView<R, C> Pt, const do
 
 // r = b - A x
 template <int R>
-__global__ void __launch_bounds__(TPB) k_bsr_residual(BsrView<R, R> A, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, TMG_BSR_MINB) k_bsr_residual(BsrView<R, R> A, const double* __restrict__ x,
                                                       const double* __restrict__ b, double* __restrict__ r) {
   TMG_PDL_ENTRY;
   int lane;
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_residual(BsrView<R, R> A, const dou
 
 // xo = x + w D^-1 (b - A x); DOT: reduce xo.b
 template <int R, bool DOT>
-__global__ void __launch_bounds__(TPB) k_bsr_jacobi(BsrView<R, R> A, const double* __restrict__ x,
+__global__ void __launch_bounds__(TPB, TMG_BSR_MINB) k_bsr_jacobi(BsrView<R, R> A, const double* __restrict__ x,
                                                     const double* __restrict__ b, const double* __restrict__ dinv,
                                                     const double* __restrict__ wp, double* __restrict__ xo, Red red) {
   TMG_PDL_ENTRY;
@@ -219,7 +229,7 @@ __global__ void k_bsr_cheb_p(const double* __restrict__ r, const double* __restr
   po[i] = beta == 0.0 ? z : z + beta * p[i];
 }
 template <int R>
-__global__ void __launch_bounds__(TPB) k_bsr_cheb(BsrView<R, R> A, const double* __restrict__ r,
+__global__ void __launch_bounds__(TPB, TMG_BSR_MINB) k_bsr_cheb(BsrView<R, R> A, const double* __restrict__ r,
                                                   const double* __restrict__ pn, const double* __restrict__ coef,
                                                   int step, int x_zero, double* __restrict__ x,
                                                   double* __restrict__ ro) {
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(TPB) k_bsr_cheb(BsrView<R, R> A, const double*
 
 // y = ds .* A (ds .* v)
 template <int R>
-__global__ void __launch_bounds__(TPB) k_bsr_apply_sym(BsrView<R, R> A, const double* __restrict__ v,
+__global__ void __launch_bounds__(TPB, TMG_BSR_MINB) k_bsr_apply_sym(BsrView<R, R> A, const double* __restrict__ v,
                                                        const double* __restrict__ ds, double* __restrict__ tmp,
                                                        double* __restrict__ y) {
   TMG_PDL_ENTRY;
