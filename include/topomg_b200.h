@@ -66,8 +66,12 @@ typedef struct {
 
 /* SolveConfig (krylov.py:17).  tmg_pcg_solve reads rtol / max_iterations; the
  * host-buffer entry tmg_solve_compliance_host also dispatches on method like
- * krylov.solve (krylov.py:146): 0 CG (extension, zero-initialised default),
- * 1 gmres_solve, 2 fgmres_solve, with restart (<= 0: the reference's 200). */
+ * SolverHarness.solve (optimization.py:90-95): 0 CG (extension, zero-initialised
+ * default of this C struct; refused with TMG_EINVAL for the non-stationary
+ * sor_chebyshev / sor_gmres smoothers), 1 gmres_solve (FGMRES when the smoother
+ * is non-stationary, as the reference), 2 fgmres_solve, with restart (<= 0: the
+ * reference's 200).  The Python SolveConfig keeps the reference's defaults
+ * (gmres, rtol 1e-7). */
 typedef struct {
   double rtol;            /* ||r|| <= rtol * ||b||, as krylov.py:63 */
   int32_t max_iterations;
@@ -75,13 +79,20 @@ typedef struct {
   int32_t restart;
 } tmg_solve_desc;
 
-/* SolveRecord (krylov.py:31). */
+/* SolveRecord (krylov.py:31).  `converged` and `final_residual` follow the
+ * reference's contract (krylov.py:124-129): the TRUE residual ||b - A x|| of the
+ * returned iterate against rtol * ||b||; residual_history ends on it.  PCG
+ * restarts from the true residual after a false convergence of its recursive
+ * residual (`restarts`). */
 typedef struct {
   int32_t iterations;
   int32_t converged;
   double initial_residual;
-  double final_residual;  /* recursive residual at exit */
-  double solve_ms;        /* device time of the solve (CUDA events) */
+  double final_residual;      /* true residual at exit */
+  double solve_ms;            /* device time of the solve (CUDA events) */
+  double recursive_residual;  /* PCG: recursively updated residual at exit (GMRES: = final) */
+  int32_t restarts;           /* PCG: cycles restarted after a false convergence (GMRES: 0) */
+  int32_t reserved;
 } tmg_solve_record;
 
 /* hierarchy level description (MgHierarchy.summary, multigrid.py:247) */

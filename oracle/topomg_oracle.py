@@ -808,9 +808,19 @@ def build_sa_amg(K, B, coarse_max_dofs, smoother=None, n_pre=1, n_post=1, seed=0
     return finalize(levels, n_pre, n_post, flags, smoother)
 
 
+def jitter(B, rel, seed=7):
+    """TEST-ONLY perturbation of SA candidates by rel (reproducibility floors: a
+    rounding-level change of the setup input)."""
+    B = np.asarray(B, float)
+    if not rel:
+        return B
+    return B * (1.0 + rel * np.random.default_rng(seed).standard_normal(B.shape))
+
+
 def build_hybrid(grid, K, B, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_post=1,
-                 seed=0, beta=BETA_DEFAULT, isolated="merge"):
-    """Geometric on the finest n_geo levels, SA below (multigrid.py:573)."""
+                 seed=0, beta=BETA_DEFAULT, isolated="merge", candidate_jitter=0.0):
+    """Geometric on the finest n_geo levels, SA below (multigrid.py:573).
+    candidate_jitter: test-only, see jitter()."""
     smoother = smoother or Smoother()
     if n_geo <= 0:
         return build_sa_amg(K, B, coarse_max_dofs, smoother, n_pre, n_post, seed, beta, isolated)
@@ -829,7 +839,7 @@ def build_hybrid(grid, K, B, n_geo, coarse_max_dofs, smoother=None, n_pre=1, n_p
         dims = coarsen_dims(dims)
         h = tuple(2 * x for x in h)
     cgrid = Grid(dims, h)
-    levels += sa_levels(A, rigid_body_modes(cgrid), coarse_max_dofs, smoother, cgrid.dpn,
+    levels += sa_levels(A, jitter(rigid_body_modes(cgrid), candidate_jitter), coarse_max_dofs, smoother, cgrid.dpn,
                         flags, seed=seed, beta=beta, isolated=isolated)
     return finalize(levels, n_pre, n_post, flags, smoother)
 
@@ -847,38 +857,57 @@ class Record:
     converged: bool = False
 
 
-def pcg(A, b, x0=None, M=None, rtol=1e-8, max_iterations=1000):
-    """EXTENSION: preconditioned CG; tolerance relative to ||b|| as the reference's
-    GMRES (krylov.py:63).  History holds the recursive residual norm per iteration."""
+def _dot(x, y):
+    return float(x @ y)
+
+
+def pcg(A, b, x0=None, M=None, rtol=1e-8, max_iterations=1000, dot=None, observe=None):
+    """EXTENSION: preconditioned CG under the reference's convergence contract.
+
+    Tolerance relative to ||b|| (krylov.py:63).  Like the reference's restarted
+    GMRES cycle (krylov.py:124-129), a cycle ends when the RECURSIVE residual
+    meets the tolerance (or the iteration cap is hit); the TRUE residual
+    ||b - A x|| then replaces the last history entry, and CG restarts from it when
+    it misses the tolerance (residual replacement).  ``converged`` is the true
+    residual test of krylov.py:128-129.
+
+    ``dot``: alternative summation order of the dot products (reproducibility
+    floors); ``observe(it, x)``: called after every iteration (fixture
+    checkpoints)."""
     t0 = time.perf_counter()
+    dot = dot or _dot
     b = np.asarray(b, float)
     x = np.zeros_like(b) if x0 is None else np.asarray(x0, float).copy()
     r = b - A @ x
-    tol = rtol * float(np.linalg.norm(b))
-    rn = float(np.linalg.norm(r))
+    tol = rtol * np.sqrt(dot(b, b))
+    rn = np.sqrt(dot(r, r))
     rec = Record(residual_history=[rn])
-    if rn <= tol:
-        rec.converged = True
-        rec.solve_time = time.perf_counter() - t0
-        return x, rec
-    z = M(r) if M is not None else r.copy()
-    p = z.copy()
-    rz = float(r @ z)
-    for it in range(1, max_iterations + 1):
-        q = A @ p
-        alpha = rz / float(p @ q)
-        x += alpha * p
-        r -= alpha * q
-        rn = float(np.linalg.norm(r))
-        rec.residual_history.append(rn)
-        rec.iterations = it
-        if rn <= tol:
-            rec.converged = True
-            break
+    it = 0
+    while rn > tol and it < max_iterations:
         z = M(r) if M is not None else r.copy()
-        rz_new = float(r @ z)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
+        p = z.copy()
+        rz = dot(r, z)
+        while True:
+            q = A @ p
+            alpha = rz / dot(p, q)
+            x += alpha * p
+            r -= alpha * q
+            rn = np.sqrt(dot(r, r))
+            it += 1
+            rec.residual_history.append(rn)
+            if observe is not None:
+                observe(it, x)
+            if rn <= tol or it >= max_iterations:
+                break
+            z = M(r) if M is not None else r.copy()
+            rz_new = dot(r, z)
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        r = b - A @ x                       # true residual (krylov.py:124-125)
+        rn = np.sqrt(dot(r, r))
+        rec.residual_history[-1] = rn
+    rec.iterations = it
+    rec.converged = bool(rn <= tol)
     rec.solve_time = time.perf_counter() - t0
     return x, rec
 

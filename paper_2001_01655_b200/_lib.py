@@ -34,7 +34,8 @@ class GmresDesc(C.Structure):
 class SolveRec(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32),
                 ("initial_residual", C.c_double), ("final_residual", C.c_double),
-                ("solve_ms", C.c_double)]
+                ("solve_ms", C.c_double), ("recursive_residual", C.c_double), ("restarts", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class LevelInfo(C.Structure):

@@ -646,6 +646,9 @@ int tmg_gmres_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* 
     rec->initial_residual = r.hist.front();
     rec->final_residual = r.hist.back();
     rec->solve_ms = r.ms;
+    rec->recursive_residual = r.hist.back();
+    rec->restarts = 0;
+    rec->reserved = 0;
   }
   ABI_END
 }
@@ -667,6 +670,9 @@ int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x,
     rec->initial_residual = r.r0;
     rec->final_residual = r.rfinal;
     rec->solve_ms = r.ms;
+    rec->recursive_residual = r.rrecursive;
+    rec->restarts = r.restarts;
+    rec->reserved = 0;
   }
   if (hist) std::memcpy(hist, r.hist.data(), r.hist.size() * sizeof(double));
   ABI_END
@@ -747,11 +753,15 @@ int tmg_solve_compliance_host(const tmg_mesh_desc* mesh, const double* rho_host,
   if (rc) return rc;
   std::unique_ptr<tmg_hierarchy> Hg(H);
   TMG_REQUIRE(cfg->method >= 0 && cfg->method <= 2, "unknown Krylov method");
+  // optimization.py:90-95: a non-stationary V-cycle (the SOR smoothers) is always
+  // run under FGMRES; the PCG extension needs a stationary symmetric one
+  const bool stationary = mg->smoother.kind <= 2;
+  TMG_REQUIRE(stationary || cfg->method != 0, "PCG needs a stationary smoother (sor_* kinds need FGMRES)");
   if (cfg->method == 0) {
     rc = tmg_pcg_solve(K, H, f.get(), u.get(), 0, cfg, nullptr, rec, s);
   } else {
     const tmg_gmres_desc g{cfg->rtol, cfg->max_iterations, cfg->restart > 0 ? cfg->restart : 200,
-                           cfg->method == 2 ? 1 : 0};
+                           (cfg->method == 2 || !stationary) ? 1 : 0};
     rc = tmg_gmres_solve(K, H, f.get(), u.get(), 0, &g, nullptr, rec, s);
   }
   if (rc) return rc;

@@ -19,10 +19,12 @@ namespace tmg {
 struct CgCfg {
   double rtol;
   int maxit;
+  int it0;  // iterations already done (restart after a false convergence)
 };
 struct CgState {
   double rz, tol;
   int it, converged, go;
+  int first;  // first iteration of a cycle (beta = 0)
 };
 
 __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ st, const double* __restrict__ bb,
@@ -32,11 +34,12 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
   const double tol = cfg->rtol * sqrt(*bb);
   const double r0 = sqrt(*rr);
   st->tol = tol;
-  st->it = 0;
+  st->it = cfg->it0;
   st->rz = 0.0;
-  hist[0] = r0;
+  st->first = 1;
+  hist[cfg->it0] = r0;  // a restart overwrites the last entry with the true residual
   st->converged = r0 <= tol;
-  st->go = (!(r0 <= tol) && cfg->maxit > 0) ? 1 : 0;
+  st->go = (!(r0 <= tol) && cfg->it0 < cfg->maxit) ? 1 : 0;
   if (use_cond) cudaGraphSetConditional(h, st->go ? 1u : 0u);
 }
 
@@ -52,7 +55,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__
   const double* __restrict__ p = odd ? P1 : P0;
   double* __restrict__ pn = odd ? P0 : P1;
   if constexpr (Op::STREAM) {
-    const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
+    const double beta = st->first ? 0.0 : (*rz_new / st->rz);
     double v = 0.0;
     fine3_rows(op, AxpySrc<DIM>{z, p, beta}, [&](int node, int, int, int, const double* o, const double* pv) {
 #pragma unroll
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__
     return;
   }
   TMG_NODE_IDX
-  const double beta = st->it == 0 ? 0.0 : (*rz_new / st->rz);
+  const double beta = st->first ? 0.0 : (*rz_new / st->rz);
   double v = 0.0;
   double out[DIM], pv[DIM];
   op.row(active, node, ci, cj, ck, AxpySrc<DIM>{z, p, beta}, out, pv);
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(TPB, 1) k_cg_update(double* __restrict__ x, do
   }
   grid_reduce((v[0] + v[1]) + (v[2] + v[3]), red, [&](double rr) {
     st->rz = *rz_new;
+    st->first = 0;
     const int it = st->it + 1;
     st->it = it;
     const double rn = sqrt(rr);
@@ -138,14 +142,14 @@ struct PcgCtx {
   DevBuf<double> b, x, r, z, p, pn, q, hist;
   DevBuf<CgCfg> cfg;
   DevBuf<CgState> st;
-  RedSlot bb, rr, rz, pq;
+  RedSlot bb, rr, rz, pq, tr;
   cudaStream_t cs = nullptr, cs2 = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // [use_x0]
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  bool use_x0_graph = false;
-  long long prologue_launches = 0, body_launches = 0;
+  long long prologue_launches[2] = {0, 0}, body_launches = 0;
   ~PcgCtx() {
-    if (exec) cudaGraphExecDestroy(exec);
+    for (auto& e : exec)
+      if (e) cudaGraphExecDestroy(e);
     if (cs) cudaStreamDestroy(cs);
     if (cs2) cudaStreamDestroy(cs2);
     if (e0) cudaEventDestroy(e0);
@@ -243,7 +247,8 @@ inline void set_coarse_l2_window(cudaStream_t s, const Hierarchy* H) {
 
 template <int DIM>
 void pcg_build_graph(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0) {
-  if (C.exec) { cudaGraphExecDestroy(C.exec); C.exec = nullptr; }
+  cudaGraphExec_t& exec = C.exec[use_x0 ? 1 : 0];
+  if (exec) { cudaGraphExecDestroy(exec); exec = nullptr; }
   cudaStream_t s = C.cs;
   set_coarse_l2_window(C.cs2, H);  // device limit: must be set outside any capture
   TMG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -270,21 +275,20 @@ void pcg_build_graph(PcgCtx& C, const Operator& K, Hierarchy* H, bool use_x0) {
   TMG_CUDA(cudaStreamBeginCaptureToGraph(C.cs2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   pcg_body<DIM>(C, K, H, C.cs2, handle, 1);
   const long long c2 = launch_counter().load();
-  C.prologue_launches = c1 - c0;
+  C.prologue_launches[use_x0 ? 1 : 0] = c1 - c0;
   C.body_launches = c2 - c1;
   note_launch(-(c2 - c0));  // captured, not executed
   cudaGraph_t body_out = nullptr;
   TMG_CUDA(cudaStreamEndCapture(C.cs2, &body_out));
   cudaGraph_t gout = nullptr;
   TMG_CUDA(cudaStreamEndCapture(s, &gout));
-  TMG_CUDA(cudaGraphInstantiate(&C.exec, gout, 0));
+  TMG_CUDA(cudaGraphInstantiate(&exec, gout, 0));
   cudaGraphDestroy(gout);
-  C.use_x0_graph = use_x0;
 }
 
 struct PcgResult {
-  int iterations = 0, converged = 0;
-  double r0 = 0, rfinal = 0, ms = 0;
+  int iterations = 0, converged = 0, restarts = 0;
+  double r0 = 0, rfinal = 0, rrecursive = 0, ms = 0;
   std::vector<double> hist;
 };
 
@@ -293,6 +297,13 @@ inline bool pcg_eager() {
   return e && e[0] == '1';
 }
 
+// The reference's convergence contract (krylov.py:124-129): a CG cycle ends when
+// the RECURSIVE residual meets rtol ||b|| (or at the cap); the TRUE residual
+// ||b - A x|| then replaces the last history entry and decides `converged`.  On
+// a false convergence CG restarts from the true residual (residual replacement,
+// the analogue of the reference's GMRES restart cycle), with the iteration count
+// and history continuing.  One extra level-0 residual + dot per cycle; the
+// restart re-enters the use_x0 graph with the iteration offset in CgCfg.
 template <int DIM>
 PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy* H, const double* b, double* x,
                     bool use_x0, double rtol, int maxit, cudaStream_t user) {
@@ -302,7 +313,6 @@ PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy*
   PcgCtx& C = *slot;
   const long long n = K.ndof;
   const bool eager = pcg_eager();
-  bool rebuild = C.exec == nullptr || C.use_x0_graph != use_x0;
   if (C.ndof != n) {
     C.ndof = n;
     const unsigned gmax = std::max({node_blocks(node_grid<DIM>(K.L)), node_blocks(row_grid<DIM, FineOp<DIM>>(K.L)), 1184u});
@@ -310,51 +320,79 @@ PcgResult pcg_solve(std::unique_ptr<PcgCtx>& slot, const Operator& K, Hierarchy*
     C.b.alloc(n, s); C.x.alloc(n, s); C.r.alloc(n, s); C.z.alloc(n, s);
     C.p.alloc(n, s); C.pn.alloc(n, s); C.q.alloc(n, s);
     C.cfg.alloc(1, s); C.st.alloc(1, s);
-    C.bb.alloc(gmax, s); C.rr.alloc(gmax, s); C.rz.alloc(gmax, s); C.pq.alloc(gmax, s);
+    C.bb.alloc(gmax, s); C.rr.alloc(gmax, s); C.rz.alloc(gmax, s); C.pq.alloc(gmax, s); C.tr.alloc(gmax, s);
     TMG_CUDA(cudaStreamCreateWithFlags(&C.cs, cudaStreamNonBlocking));
     TMG_CUDA(cudaStreamCreateWithFlags(&C.cs2, cudaStreamNonBlocking));
     TMG_CUDA(cudaEventCreate(&C.e0));
     TMG_CUDA(cudaEventCreate(&C.e1));
-    rebuild = true;
+    for (auto& e : C.exec)
+      if (e) { cudaGraphExecDestroy(e); e = nullptr; }
   }
   if (maxit + 1 > C.hist_cap) {
     C.hist_cap = std::max(maxit + 1, 1024);
     C.hist.alloc(C.hist_cap, user);
-    rebuild = true;
+    for (auto& e : C.exec)
+      if (e) { cudaGraphExecDestroy(e); e = nullptr; }
   }
-  if (rebuild && !eager) {
-    TMG_CUDA(cudaStreamSynchronize(user));  // buffers allocated on `user` must exist before capture
-    pcg_build_graph<DIM>(C, K, H, use_x0);
-  }
-  CgCfg hc{rtol, maxit};
+  auto op0 = K.template fine<DIM>();
+  const unsigned gv = red_grid(n);
+  CgCfg hc{rtol, maxit, 0};
   CgState hs;
+  PcgResult res;
   TMG_CUDA(cudaEventRecord(C.e0, user));
-  TMG_CUDA(cudaMemcpyAsync(C.cfg.get(), &hc, sizeof(hc), cudaMemcpyHostToDevice, user));
   TMG_CUDA(cudaMemcpyAsync(C.b.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, user));
   if (use_x0) TMG_CUDA(cudaMemcpyAsync(C.x.get(), x, n * sizeof(double), cudaMemcpyDeviceToDevice, user));
-  if (eager) {
-    pcg_prologue<DIM>(C, K, H, use_x0, user, 0, 0);
-    while (true) {
-      TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
-      TMG_CUDA(cudaStreamSynchronize(user));
-      if (!hs.go) break;
-      pcg_body<DIM>(C, K, H, user, 0, 0);
+  bool x0 = use_x0;
+  double tnorm = 0.0;
+  for (;;) {
+    TMG_CUDA(cudaMemcpyAsync(C.cfg.get(), &hc, sizeof(hc), cudaMemcpyHostToDevice, user));
+    if (eager) {
+      pcg_prologue<DIM>(C, K, H, x0, user, 0, 0);
+      while (true) {
+        TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
+        TMG_CUDA(cudaStreamSynchronize(user));
+        if (!hs.go) break;
+        pcg_body<DIM>(C, K, H, user, 0, 0);
+      }
+    } else {
+      cudaGraphExec_t& ex = C.exec[x0 ? 1 : 0];
+      if (!ex) {
+        TMG_CUDA(cudaStreamSynchronize(user));  // buffers allocated on `user` must exist before capture
+        pcg_build_graph<DIM>(C, K, H, x0);
+      }
+      TMG_CUDA(cudaGraphLaunch(ex, user));
     }
-  } else {
-    TMG_CUDA(cudaGraphLaunch(C.exec, user));
+    // true residual of the cycle's iterate (C.z is free between cycles)
+    launch(k_residual<DIM, decltype(op0)>, TMG_ROW_OP_LAUNCH_L(K.L, op0), user, op0, C.x.get(), C.b.get(),
+           C.z.get());
+    launch(k_dot, gv, TPB, 0, user, C.z.get(), C.z.get(), n, C.tr.red());
+    note_launch(2);
+    TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
+    double trr = 0.0;
+    TMG_CUDA(cudaMemcpyAsync(&trr, C.tr.res.get(), sizeof(double), cudaMemcpyDeviceToHost, user));
+    TMG_CUDA(cudaStreamSynchronize(user));
+    if (!eager) note_launch(C.prologue_launches[x0 ? 1 : 0] + (long long)(hs.it - hc.it0) * C.body_launches);
+    const int done = hs.it;
+    if (res.hist.size() < (size_t)done + 1) res.hist.resize(done + 1);
+    TMG_CUDA(cudaMemcpy(res.hist.data() + hc.it0, C.hist.get() + hc.it0, (done - hc.it0 + 1) * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    res.rrecursive = res.hist[done];
+    tnorm = std::sqrt(trr);
+    res.hist[done] = tnorm;  // krylov.py:125: the history ends on the true residual
+    if (tnorm <= hs.tol || done >= maxit) break;
+    // false convergence (recursive residual met the tolerance, the true one does
+    // not): restart from the true residual
+    hc.it0 = done;
+    x0 = true;
+    ++res.restarts;
   }
   TMG_CUDA(cudaMemcpyAsync(x, C.x.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, user));
   TMG_CUDA(cudaEventRecord(C.e1, user));
-  TMG_CUDA(cudaMemcpyAsync(&hs, C.st.get(), sizeof(hs), cudaMemcpyDeviceToHost, user));
   TMG_CUDA(cudaStreamSynchronize(user));
-  if (!eager) note_launch(C.prologue_launches + (long long)hs.it * C.body_launches);
-  PcgResult res;
   res.iterations = hs.it;
-  res.converged = hs.converged;
-  res.hist.resize(hs.it + 1);
-  TMG_CUDA(cudaMemcpy(res.hist.data(), C.hist.get(), (hs.it + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+  res.converged = tnorm <= hs.tol;
   res.r0 = res.hist.front();
-  res.rfinal = res.hist.back();
+  res.rfinal = tnorm;
   float ms = 0.f;
   TMG_CUDA(cudaEventElapsedTime(&ms, C.e0, C.e1));
   res.ms = ms;

@@ -19,8 +19,11 @@ from ._dev import as_dev, empty_dev, ptr, stream_ptr
 
 @dataclass(frozen=True)
 class SolveConfig:
-    method: str = "cg"  # cg (north-star PCG) | gmres | fgmres (reference krylov.py:17)
-    rtol: float = 1e-8
+    """krylov.py:17-19 with the reference's defaults (gmres, rtol 1e-7).  The
+    north-star PCG is selected explicitly with method="cg" (or by calling
+    cg_solve); a default config therefore runs what the reference runs."""
+    method: str = "gmres"  # gmres | fgmres (reference) | cg (EXTENSION: the north-star PCG)
+    rtol: float = 1e-7
     max_iterations: int = 1000
     restart: int = 200
 
@@ -33,11 +36,18 @@ class SolveConfig:
 
 @dataclass
 class SolveRecord:
+    """krylov.py:28-34.  ``converged`` is the reference's TRUE residual test
+    (||b - A x|| <= rtol ||b||, krylov.py:128-129) and residual_history ends on
+    that true residual.  Extensions: ``recursive_residual`` (PCG's recursively
+    updated residual at exit) and ``restarts`` (PCG cycles restarted from the
+    true residual after a false convergence)."""
     iterations: int = 0
     setup_time: float = 0.0
     solve_time: float = 0.0
     residual_history: list = field(default_factory=list)
     converged: bool = False
+    recursive_residual: float = 0.0
+    restarts: int = 0
 
     def csv_row(self):
         final = self.residual_history[-1] if self.residual_history else 0.0
@@ -47,8 +57,10 @@ class SolveRecord:
 
 def cg_solve(A, b, x0=None, M=None, cfg=None, out=None, stream=None):
     """Preconditioned CG on the device.  A: StiffnessOperator; M: MgHierarchy or
-    None.  Returns (x, SolveRecord); x is a CUDA fp64 tensor."""
-    cfg = cfg or SolveConfig()
+    None (a stationary, symmetric preconditioner).  Returns (x, SolveRecord); x
+    is a CUDA fp64 tensor.  Convergence follows the reference's true-residual
+    contract (krylov.py:124-129): see SolveRecord."""
+    cfg = cfg or SolveConfig(method="cg")
     b = as_dev(b)
     n = A.shape[0]
     if b.numel() != n:
@@ -64,7 +76,8 @@ def cg_solve(A, b, x0=None, M=None, cfg=None, out=None, stream=None):
                                          C.byref(rec), stream_ptr(stream)))
     record = SolveRecord(iterations=int(rec.iterations), solve_time=rec.solve_ms / 1e3,
                          residual_history=list(hist[:rec.iterations + 1]),
-                         converged=bool(rec.converged))
+                         converged=bool(rec.converged), recursive_residual=float(rec.recursive_residual),
+                         restarts=int(rec.restarts))
     return x, record
 
 
@@ -86,7 +99,8 @@ def _gmres(A, b, x0, M, cfg, flexible, stream=None):
                                            1 if x0 is not None else 0, C.byref(desc), hist.ctypes.data,
                                            C.byref(rec), stream_ptr(stream)))
     return x, SolveRecord(iterations=int(rec.iterations), solve_time=rec.solve_ms / 1e3,
-                          residual_history=list(hist[:rec.iterations + 1]), converged=bool(rec.converged))
+                          residual_history=list(hist[:rec.iterations + 1]), converged=bool(rec.converged),
+                          recursive_residual=float(rec.final_residual))
 
 
 def gmres_solve(A, b, x0=None, M=None, cfg=None):
@@ -100,8 +114,8 @@ def fgmres_solve(A, b, x0=None, M=None, cfg=None):
 
 
 def solve(A, b, x0=None, M=None, cfg=None):
-    """Dispatch on cfg.method (krylov.py:146): 'cg' (the north-star PCG),
-    'gmres', 'fgmres'."""
+    """Dispatch on cfg.method (krylov.py:146): 'gmres' (default), 'fgmres', and
+    the extension 'cg' (the north-star PCG)."""
     cfg = cfg or SolveConfig()
     if cfg.method == "cg":
         return cg_solve(A, b, x0, M, cfg)

@@ -47,7 +47,11 @@ class SmootherConfig:
 
     @property
     def stationary(self):
-        return self.kind in ("weighted_jacobi", "block_jacobi")
+        """True if repeated application is a fixed linear operator (multigrid.py:43).
+        The extension kind "chebyshev" (Jacobi-Chebyshev with fixed Lanczos-bound
+        coefficients) is a fixed symmetric polynomial in D^-1 A, hence stationary;
+        the reference's SOR-based kinds are not."""
+        return self.kind in ("weighted_jacobi", "block_jacobi", "chebyshev")
 
     def desc(self, ndofs=0):
         """C-ABI descriptor.  sor_chebyshev carries its power-method start vector

@@ -73,10 +73,27 @@ class SolverHarness:
         return h, time.perf_counter() - t0
 
     def solve(self, K, f, x0=None, hierarchy=None):
+        """Solve K x = f; returns (x, SolveRecord, hierarchy) (optimization.py:85).
+        As the reference (optimization.py:90-95): GMRES for a stationary
+        preconditioner unless FGMRES is asked for, FGMRES otherwise (the
+        sor_chebyshev / sor_gmres smoothers).  method="cg" (the north-star PCG)
+        needs a stationary symmetric V-cycle and is refused for the others."""
         setup = 0.0
         if hierarchy is None and self.strategy != "none":
             hierarchy, setup = self.build(K)
-        x, rec = krylov.solve(K, f, x0, hierarchy, self.solve_cfg)
+        stationary = hierarchy is None or hierarchy.stationary
+        method = self.solve_cfg.method
+        if method == "cg":
+            if not stationary:
+                raise ValueError("method='cg' needs a stationary preconditioner; the %s smoother is not "
+                                 "(use 'gmres' -> FGMRES, as the reference)" % hierarchy.smoother_config.kind)
+            x, rec = krylov.cg_solve(K, f, x0, hierarchy, self.solve_cfg)
+        elif method not in ("gmres", "fgmres"):
+            raise ValueError("unknown Krylov method %r" % method)
+        elif stationary and method != "fgmres":
+            x, rec = krylov.gmres_solve(K, f, x0, hierarchy, self.solve_cfg)
+        else:
+            x, rec = krylov.fgmres_solve(K, f, x0, hierarchy, self.solve_cfg)
         rec.setup_time = setup
         if self.strategy == "hybrid_adaptive":
             adapt_after_solve(self.controller, rec.iterations)

@@ -1,0 +1,45 @@
+"""Shared helpers of the fixed-iteration checkpoint fixtures (test infrastructure).
+
+A full-size iterate (0.6-5.4 M doubles) is too large for a fixture, so every
+checkpoint stores the compliance f.x_k, ||x_k|| and x_k projected on NPROJ
+seeded Gaussian vectors.  For Gaussian W, ||W(x - y)|| / ||W y|| estimates
+||x - y|| / ||y|| (relative spread ~ 1/sqrt(2 NPROJ)), so a device iterate is
+compared with the oracle's without storing either.
+
+Used by tests/golden/make_checkpoints.py (writes the fixtures on the CPU) and
+tests/test_gpu_configs.py (checks the device against them)."""
+
+import numpy as np
+
+NPROJ = 16
+PROJ_SEED = 20010165
+# iterations at which the iterates are pinned, per config (capped by each run)
+CHECKPOINTS = (10, 50, 200, 1000, 2000, 3000)
+
+
+def project(x, nproj=NPROJ, seed=PROJ_SEED):
+    """W x for W = default_rng(seed + i).standard_normal(n), row by row (no n x
+    nproj matrix in memory)."""
+    x = np.asarray(x, dtype=float)
+    return np.array([np.random.default_rng(seed + i).standard_normal(x.size) @ x for i in range(nproj)])
+
+
+def proj_rel(px, py):
+    """||W x - W y|| / ||W y||: estimate of ||x - y|| / ||y||."""
+    return float(np.linalg.norm(np.asarray(px) - np.asarray(py)) / np.linalg.norm(py))
+
+
+def block_dot(x, y, nblk=296):
+    """The GPU's two-level reduction order (296 block partials, then their sum)."""
+    return float(sum(np.add.reduce(c) for c in np.array_split(x * y, nblk)))
+
+
+class Transposed:
+    """K^T @ x: the same (symmetric) operator with another fp64 summation order."""
+
+    def __init__(self, K):
+        self.KT = K.T.tocsr()
+        self.shape = K.shape
+
+    def __matmul__(self, x):
+        return self.KT @ x

@@ -1,0 +1,169 @@
+"""Fixed-iteration oracle checkpoints of the FULL BASELINE configs (test
+infrastructure, CPU, build container).
+
+    python tests/golden/make_checkpoints.py run --config C --variant base|perturbed [--maxit N]
+    python tests/golden/make_checkpoints.py combine --config C
+
+`run` builds the config's hierarchy with the oracle and runs its PCG (the
+reference's true-residual contract, oracle.pcg) for every leg, recording at
+the checkpoints k of tests/ckpt_common.CHECKPOINTS the compliance f.x_k,
+||x_k||, the true residual ||f - K x_k|| and x_k projected on 16 seeded
+Gaussian vectors; the iterates themselves go to a scratch directory.
+
+`perturbed` is the same oracle with only rounding-level changes: the matvec
+summed in the transposed order (K^T @ x), the dots in the GPU's 296-block
+order, and (SA levels of 3D problems) the rigid-mode candidates jittered by
+1e-14 -- the reproducibility floor of each observable.
+
+`combine` writes tests/golden/config{C}_checkpoints.npz: the base run's
+observables, and per checkpoint the EXACT base-vs-perturbed distance of the
+iterates and of the compliance (the floors).  tests/test_gpu_configs.py checks
+the device against the base run with tolerance max(north-star, 10 x floor)."""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import ckpt_common as CK  # noqa: E402
+from oracle import topomg_oracle as O  # noqa: E402
+from paper_2001_01655_b200 import problems as P  # noqa: E402
+
+SCRATCH = os.environ.get("TMG_CKPT_SCRATCH", "/tmp/tmg_ckpt")
+# iteration caps of the fixed-iteration runs (the configs that converge run to
+# convergence under the cap)
+MAXIT = {1: 2000, 2: 3000, 3: 3000, 4: 200}
+JITTER = 1e-14
+
+
+def leg_tag(leg):
+    return P.leg_name(leg).replace("+", "_")
+
+
+def build(c, w, g, K, leg, perturbed):
+    jit = JITTER if (perturbed and len(w.mesh.dims) == 3) else 0.0
+    if leg["smoother"] == "chebyshev":
+        sm = O.Smoother("chebyshev", 1.0, leg["degree"], lanczos_steps=leg["lanczos_steps"])
+    else:
+        sm = O.Smoother(leg["smoother"], leg["weight"], safeguard=leg.get("safeguard", 0.0))
+    if leg["strategy"] == "gmg":
+        return O.build_gmg(g, K, 1, sm, leg["n_pre"], leg["n_post"], max_levels=leg["levels"])
+    if leg["strategy"] == "amg":
+        B = O.jitter(O.rigid_body_modes(g, w.bc.fixed_dofs), jit)
+        return O.build_sa_amg(K, B, leg["coarse_max_dofs"], sm, leg["n_pre"], leg["n_post"], beta=leg["beta"],
+                              isolated=leg.get("isolated", "merge"))
+    return O.build_hybrid(g, K, O.rigid_body_modes(g, w.bc.fixed_dofs), leg["n_geo"], leg["coarse_max_dofs"], sm,
+                          leg["n_pre"], leg["n_post"], beta=leg["beta"], isolated=leg.get("isolated", "merge"),
+                          candidate_jitter=jit)
+
+
+def _lmax(lv):
+    v = getattr(lv.smoother, "lmax_estimate", None) if lv.smoother is not None else None
+    return np.nan if v is None else float(v)
+
+
+def run(c, variant, maxit):
+    os.makedirs(SCRATCH, exist_ok=True)
+    perturbed = variant == "perturbed"
+    t0 = time.time()
+    w = P.CONFIGS[c]()
+    g = O.make_grid(w.mesh.dims)
+    E = O.simp_modulus(w.rho, P.PENAL, P.E0, P.EMIN)
+    K = O.assemble_stiffness(g, w.bc.fixed_dofs, E)
+    A = CK.Transposed(K) if perturbed else K
+    dot = CK.block_dot if perturbed else None
+    print("config %d %s: assembly %.1f s" % (c, variant, time.time() - t0), flush=True)
+    loads = [w.bc.load_vector] + list(w.loads)
+    for leg in w.solvers:
+        t1 = time.time()
+        h = build(c, w, g, K, leg, perturbed)
+        tag = leg_tag(leg)
+        print("  %s: setup %.1f s, levels %s" % (tag, time.time() - t1, [lv.A.shape[0] for lv in h.levels]),
+              flush=True)
+        cap = min(maxit, leg.get("max_iterations", maxit))
+        for li, f in enumerate(loads):
+            obs = {}
+            ks = [k for k in CK.CHECKPOINTS if k <= cap]
+
+            def observe(it, x, obs=obs, ks=ks, f=f, tag=tag, li=li):
+                if it in ks:
+                    np.save(os.path.join(SCRATCH, "c%d_%s_l%d_%s_x%d.npy" % (c, tag, li, variant, it)), x)
+                    obs[it] = (float(f @ x), float(np.linalg.norm(x)), float(np.linalg.norm(f - K @ x)),
+                               CK.project(x))
+                    print("    it %d: compliance %.12e |x| %.6e true res %.3e" % (it, *obs[it][:3]), flush=True)
+
+            t2 = time.time()
+            x, rec = O.pcg(A, f, None, h.apply, rtol=w.rtol, max_iterations=cap, dot=dot, observe=observe)
+            np.save(os.path.join(SCRATCH, "c%d_%s_l%d_%s_xfinal.npy" % (c, tag, li, variant)), x)
+            out = dict(sizes=np.array([lv.A.shape[0] for lv in h.levels]),
+                       lmax=np.array([_lmax(lv) for lv in h.levels[:-1]], dtype=float),
+                       hist=np.array(rec.residual_history), iterations=rec.iterations, converged=rec.converged,
+                       ks=np.array(sorted(obs)), comp=np.array([obs[k][0] for k in sorted(obs)]),
+                       xnorm=np.array([obs[k][1] for k in sorted(obs)]),
+                       tres=np.array([obs[k][2] for k in sorted(obs)]),
+                       proj=np.array([obs[k][3] for k in sorted(obs)]).reshape(len(obs), CK.NPROJ),
+                       final_comp=float(f @ x), final_xnorm=float(np.linalg.norm(x)), final_proj=CK.project(x),
+                       fnorm=float(np.linalg.norm(f)))
+            np.savez(os.path.join(SCRATCH, "c%d_%s_l%d_%s.npz" % (c, tag, li, variant)), **out)
+            print("  %s load %d: %d iterations in %.1f s, converged %s, true rel. res %.3e" % (
+                tag, li, rec.iterations, time.time() - t2, rec.converged,
+                rec.residual_history[-1] / np.linalg.norm(f)), flush=True)
+    print("config %d %s done in %.1f s" % (c, variant, time.time() - t0), flush=True)
+
+
+def combine(c):
+    w = P.CONFIGS[c]()
+    loads = 1 + len(w.loads)
+    out = {}
+    for leg in w.solvers:
+        tag = leg_tag(leg)
+        for li in range(loads):
+            key = "%s_l%d" % (tag, li)
+            b = dict(np.load(os.path.join(SCRATCH, "c%d_%s_base.npz" % (c, key))))
+            p = dict(np.load(os.path.join(SCRATCH, "c%d_%s_perturbed.npz" % (c, key))))
+            fx, fc = [], []
+            for k in b["ks"]:
+                xb = np.load(os.path.join(SCRATCH, "c%d_%s_base_x%d.npy" % (c, key, k)))
+                xp = np.load(os.path.join(SCRATCH, "c%d_%s_perturbed_x%d.npy" % (c, key, k)))
+                fx.append(np.linalg.norm(xp - xb) / np.linalg.norm(xb))
+                fc.append(abs(p["comp"][list(p["ks"]).index(k)] - b["comp"][list(b["ks"]).index(k)])
+                          / abs(b["comp"][list(b["ks"]).index(k)]))
+            xb = np.load(os.path.join(SCRATCH, "c%d_%s_base_xfinal.npy" % (c, key)))
+            xp = np.load(os.path.join(SCRATCH, "c%d_%s_perturbed_xfinal.npy" % (c, key)))
+            for name, v in b.items():
+                out["%s_%s" % (key, name)] = v
+            out[key + "_floor_x"] = np.array(fx)
+            out[key + "_floor_comp"] = np.array(fc)
+            out[key + "_floor_final_x"] = np.array(np.linalg.norm(xp - xb) / np.linalg.norm(xb))
+            out[key + "_floor_final_comp"] = np.array(abs(p["final_comp"] - b["final_comp"]) / abs(b["final_comp"]))
+            out[key + "_perturbed_iterations"] = p["iterations"]
+            out[key + "_perturbed_hist"] = p["hist"]
+            print(key, "iterations base %d perturbed %d" % (b["iterations"], p["iterations"]),
+                  "floors x", np.array2string(np.array(fx), precision=2), "comp",
+                  np.array2string(np.array(fc), precision=2))
+    path = os.path.join(HERE, "config%d_checkpoints.npz" % c)
+    np.savez_compressed(path, **out)
+    print("wrote", path)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["run", "combine"])
+    ap.add_argument("--config", type=int, required=True)
+    ap.add_argument("--variant", choices=["base", "perturbed"], default="base")
+    ap.add_argument("--maxit", type=int, default=None)
+    a = ap.parse_args()
+    if a.cmd == "run":
+        run(a.config, a.variant, a.maxit or MAXIT[a.config])
+    else:
+        combine(a.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -112,7 +112,8 @@ def test_adaptive_hybrid_controller_host_logic():
 
 def test_solve_config_validation_and_methods():
     from paper_2001_01655_b200 import SolveConfig
-    assert SolveConfig().method == "cg"
+    # the reference's defaults (krylov.py:17-19); the north-star PCG is opt-in
+    assert (SolveConfig().method, SolveConfig().rtol, SolveConfig().restart) == ("gmres", 1e-7, 200)
     for bad in (dict(rtol=0.0), dict(rtol=1.0), dict(restart=0)):
         with pytest.raises(ValueError):
             SolveConfig(**bad)
@@ -131,6 +132,8 @@ def test_smoother_descriptor_host_logic():
     assert np.array_equal(ps, np.random.default_rng(0).standard_normal(257))
     assert not SmootherConfig(kind="sor_gmres").desc(10).power_start
     assert not SmootherConfig(kind="sor_gmres").stationary and SmootherConfig().stationary
+    assert not SmootherConfig(kind="sor_chebyshev").stationary
+    assert SmootherConfig(kind="chebyshev", weight=1.0).stationary  # fixed polynomial in D^-1 A
     with pytest.raises(ValueError):
         SmootherConfig(kind="sor").desc(10)
     with pytest.raises(ValueError):
@@ -145,3 +148,39 @@ def test_solve_descriptor_defaults_to_cg():
     assert (d.method, d.restart) == (0, 0)
     d = L.SolveDesc(1e-8, 100, 2, 7)
     assert (d.method, d.restart) == (2, 7)
+
+
+def test_harness_routes_like_the_reference(monkeypatch):
+    """optimization.py:90-95: GMRES for a stationary preconditioner unless FGMRES
+    is asked for, FGMRES for the SOR smoothers; method="cg" refuses a
+    non-stationary V-cycle (host logic only, the Krylov drivers are stubbed)."""
+    import paper_2001_01655_b200 as T
+    from paper_2001_01655_b200 import krylov
+
+    calls = []
+    for name in ("cg_solve", "gmres_solve", "fgmres_solve"):
+        monkeypatch.setattr(krylov, name, lambda *a, _n=name, **k: (calls.append(_n) or (None, krylov.SolveRecord())))
+
+    class H:
+        def __init__(self, kind):
+            self.smoother_config = T.SmootherConfig(kind=kind)
+
+        @property
+        def stationary(self):
+            return self.smoother_config.stationary
+
+    mesh = T.build_mesh((4, 2))
+    for kind, method, want in (("weighted_jacobi", "gmres", "gmres_solve"), ("weighted_jacobi", "fgmres", "fgmres_solve"),
+                               ("sor_gmres", "gmres", "fgmres_solve"), ("sor_chebyshev", "gmres", "fgmres_solve"),
+                               ("weighted_jacobi", "cg", "cg_solve")):
+        hs = T.SolverHarness(mesh, strategy="gmg", solve_cfg=T.SolveConfig(method=method))
+        calls.clear()
+        hs.solve(None, None, hierarchy=H(kind))
+        assert calls == [want], (kind, method, calls)
+    hs = T.SolverHarness(mesh, strategy="gmg", solve_cfg=T.SolveConfig(method="cg"))
+    with pytest.raises(ValueError):
+        hs.solve(None, None, hierarchy=H("sor_gmres"))
+    hs = T.SolverHarness(mesh, strategy="none", solve_cfg=T.SolveConfig())
+    calls.clear()
+    hs.solve(None, None)
+    assert calls == ["gmres_solve"]

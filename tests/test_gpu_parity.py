@@ -240,7 +240,7 @@ def test_compliance_and_sensitivity_config0():
     law = T.SimpLaw(penalty=3.0, e_min_ratio=1e-9)
     harness = T.SolverHarness(mesh=w.mesh, strategy="gmg", coarse_max_dofs=1,
                               smoother=T.SmootherConfig(weight=0.6), n_pre=2, n_post=2, max_levels=3,
-                              solve_cfg=T.SolveConfig(rtol=1e-8))
+                              solve_cfg=T.SolveConfig(method="cg", rtol=1e-8))
     F, dF, aux = T.compliance_and_sensitivity(w.mesh, w.bc, None, law, w.rho, harness)
     Kref = O.assemble_stiffness(g, w.bc.fixed_dofs, w.moduli)
     ho = O.build_gmg(g, Kref, 1, O.Smoother(weight=0.6), 2, 2, max_levels=3)
