@@ -186,6 +186,12 @@ int tmg_operator_create(const tmg_mesh_desc* mesh, const double* element_moduli_
   o.ndof = o.L.n * o.dim;
   o.nu = nu;
   o.ke_host = element_stiffness(o.dim, o.h, 1.0, nu);
+  if (o.dim == 3) {
+    o.keh_host.assign(f3h::NZ, 0.0);
+    // the box element's mirror symmetry puts KE in 8 character blocks (45 terms)
+    TMG_REQUIRE(f3h::hat_coefficients(o.ke_host.data(), o.keh_host.data()) <= 1e-12,
+                "element matrix lacks the mirror symmetry of a box element");
+  }
   std::vector<uint8_t> mask(o.L.n, (uint8_t)((1u << o.dim) - 1u));
   for (int64_t t = 0; t < n_fixed; ++t) {
     const int64_t d = fixed_dofs_host[t];

@@ -1,5 +1,5 @@
 // Hex8 matrix-free operator rows, two x-adjacent nodes per thread (A/B build
-// option -DTMG_FINE3_PAIR; the default 3D path is the FineOp::row tile).
+// option -DTMG_FINE3_PAIR; the default 3D path is tmg_fine3h.cuh).
 //
 // The 3D level-0 product K u (mesh.py:327, Z K Z + I_fixed) costs 576 FMA per
 // node (24 x 24 KE per element) against ~104 B of HBM traffic: on B200 it is
@@ -36,7 +36,7 @@ inline dim3 grid(const Lat& L) {
 // out = row of Z K Z + I_fixed applied to the source, self = source at the node.
 // Called by all threads of the block.
 template <class Src, class Epi>
-__device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, Epi&& epi) {
+__device__ __forceinline__ void fine3_pair_rows(const FineOp<3>& op, const Src& src, Epi&& epi) {
   using namespace f3;
   extern __shared__ __align__(16) double f3_sm[];
   double* xs = f3_sm;          // masked source, [node][3]

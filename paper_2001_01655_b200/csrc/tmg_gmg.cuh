@@ -728,7 +728,9 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
     const char* e = std::getenv("TMG_FUSE_PROLONG");
     return e ? std::atoi(e) : 0;  // measured: unfused is faster on every level
   }();
+  // (not on a streamed 3D level 0: its row kernels have their own launch shape)
   const bool fuse_prolong = !cheb && H.sm.kind == SM_JACOBI && H.n_post > 0 && l.xfer == XF_GEO && l.lattice() &&
+                            !(DIM == 3 && l.opkind == OP_FINE) &&
                             (fuse_mode == 2 || (fuse_mode == 1 && l.opkind == OP_FINE));
   if (!fuse_prolong) xfer_prolong_add<DIM>(H, k, xcur, s);
   if (cheb) {

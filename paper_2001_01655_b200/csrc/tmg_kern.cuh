@@ -173,6 +173,7 @@ struct Operator {
   DevBuf<double> E, ke;
   DevBuf<uint8_t> mask;
   std::vector<double> ke_host;
+  std::vector<double> keh_host;  // 3D: KE in the reflection-character basis (tmg_fine3h.cuh)
   template <int DIM>
   FineOp<DIM> fine() const {
     FineOp<DIM> o;
@@ -181,6 +182,7 @@ struct Operator {
     o.E = E.get();
     o.mask = mask.get();
     std::memcpy(o.ke, ke_host.data(), sizeof(o.ke));
+    if constexpr (DIM == 3) std::memcpy(o.keh, keh_host.data(), sizeof(o.keh));
     return o;
   }
 };

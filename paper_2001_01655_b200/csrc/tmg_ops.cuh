@@ -229,6 +229,7 @@ struct FineOp {
   const double* __restrict__ E;
   const uint8_t* __restrict__ mask;  // bit c set -> dof c of the node is free
   double ke[NE * NE];                // kernel-parameter constant bank
+  double keh[DIM == 3 ? 45 : 1];     // 3D: KE in the reflection-character basis (tmg_fine3h.cuh)
 
   __device__ int elem_id(int ex, int ey, int ez) const { return ex + ne[0] * (ey + ne[1] * ez); }
 
@@ -262,14 +263,23 @@ struct FineOp {
 #ifndef TMG_F2_MINB
 #define TMG_F2_MINB 5  // 2D: 48 registers, 5 CTAs per SM (measured: sweep 5.82 -> 5.45 us vs 4 / 6 CTAs)
 #endif
-  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
-  // 3D pair rows (tmg_fine3.cuh, fine3_rows: two x-adjacent nodes per thread)
-  // are an A/B build option (-DTMG_FINE3_PAIR); measured on par with the tile
-  // (201 vs 194 us per config-4 sweep), so the tile stays the default.
-#ifdef TMG_FINE3_PAIR
-  static constexpr bool STREAM = DIM == 3;
-#else
+#ifndef TMG_F3H_MINB
+#define TMG_F3H_MINB 2  // 3D character-basis stream: 128 registers (no spills), 2 CTAs per SM
+#endif
+  // 3D rows are streamed (STREAM: one launch shape for every 3D level-0 kernel):
+  // by default the element-centric character-basis operator of tmg_fine3h.cuh
+  // (~175 FP64 operations per element instead of 576); -DTMG_FINE3_PAIR selects
+  // the two-nodes-per-thread gather of tmg_fine3.cuh, -DTMG_FINE3_TILE the
+  // node-per-thread tile below (row()) -- both kept as measured A/B baselines.
+#ifdef TMG_FINE3_TILE
   static constexpr bool STREAM = false;
+#else
+  static constexpr bool STREAM = DIM == 3;
+#endif
+#if defined(TMG_FINE3_TILE) || defined(TMG_FINE3_PAIR)
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
+#else
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;
 #endif
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
@@ -489,7 +499,39 @@ struct FineOp {
 
 }  // namespace tmg
 #include "tmg_fine3.cuh"
+#include "tmg_fine3h.cuh"
 namespace tmg {
+// the streamed 3D row path (FineOp<3>::STREAM): character-basis elements
+// (default) or the two-nodes-per-thread gather (-DTMG_FINE3_PAIR)
+template <class Src, class Epi>
+__device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, Epi&& epi) {
+#ifdef TMG_FINE3_PAIR
+  fine3_pair_rows(op, src, static_cast<Epi&&>(epi));
+#else
+  fine3h_rows(op, src, static_cast<Epi&&>(epi));
+#endif
+}
+inline dim3 fine3_grid(const Lat& L) {
+#ifdef TMG_FINE3_PAIR
+  return f3::grid(L);
+#else
+  return f3h::grid(L);
+#endif
+}
+constexpr int fine3_threads() {
+#ifdef TMG_FINE3_PAIR
+  return f3::NT;
+#else
+  return f3h::NT;
+#endif
+}
+constexpr size_t fine3_smem() {
+#ifdef TMG_FINE3_PAIR
+  return f3::SMEM_BYTES;
+#else
+  return f3h::SMEM_BYTES;
+#endif
+}
 
 // ----------------------------------------------------------------------------
 // StencilOp
@@ -596,17 +638,17 @@ struct StencilOp {
 // launch one CTA per 16x16 node column and z-chunk, the others one thread per node
 template <int DIM, class Op>
 inline dim3 row_grid(const Lat& L) {
-  if constexpr (Op::STREAM) return f3::grid(L);
+  if constexpr (Op::STREAM) return fine3_grid(L);
   else return dim3((L.nn[0] + Op::BX - 1) / Op::BX, (L.nn[1] + Op::BY - 1) / Op::BY, (L.nn[2] + Op::BZ - 1) / Op::BZ);
 }
 template <int DIM, class Op>
 inline dim3 row_block() {
-  if constexpr (Op::STREAM) return dim3(f3::NT, 1, 1);
+  if constexpr (Op::STREAM) return dim3(fine3_threads(), 1, 1);
   else return dim3(Op::BX, Op::BY, Op::BZ);
 }
 template <class Op>
 constexpr size_t row_smem() {
-  if constexpr (Op::STREAM) return f3::SMEM_BYTES;
+  if constexpr (Op::STREAM) return fine3_smem();
   else return Op::SMEM_BYTES;
 }
 #define TMG_ROW_OP_LAUNCH_L(Lat_, op_) \

@@ -16,7 +16,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2001_01655_b200 as T  # noqa: E402
-from test_gpu_parity import (cantilever, host, iteration_tolerance, rel,  # noqa: E402
+from test_gpu_parity import (assert_pcg_parity, cantilever, host, iteration_tolerance, rel,  # noqa: E402
                              reproducibility_floor)
 
 
@@ -88,12 +88,8 @@ def test_amg_pcg_matches_oracle(dims, beta, isolated):
     ho = oracle_sa(g, Kref, bc.fixed_dofs, 60, beta, O.Smoother(weight=0.6), isolated=isolated)
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
-    assert rec.converged and reco.converged
-    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
-    assert abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
-    assert rel(host(u), uo) <= max(1e-8, 10 * fu)
-    c, co = float(bc.load_vector @ host(u)), float(bc.load_vector @ uo)
-    assert abs(c - co) <= max(1e-10, 10 * fc) * abs(co)
+    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000))
 
 
 # (16,8,8) with n_geo=2 is deliberately absent: its second SA level aggregates two
@@ -101,9 +97,15 @@ def test_amg_pcg_matches_oracle(dims, beta, isolated):
 # R's diagonal from the 2-node aggregates above), so the trailing Householder
 # columns of T are rounding noise in ANY implementation -- the reference is not
 # reproducible there either (tests/diagnostics/debug_hybrid.py shows the level-by-level split).
-@pytest.mark.parametrize("dims,n_geo,kind", [((16, 8, 8), 1, "weighted_jacobi"), ((16, 8, 8), 1, "chebyshev"),
-                                             ((32, 16), 2, "weighted_jacobi"), ((24, 12, 12), 2, "chebyshev")])
-def test_hybrid_matches_oracle(dims, n_geo, kind):
+# (32,16): |u| = 3.6e8 with |f| = 1, so the fp64 floor of the TRUE residual,
+# ~eps |K| |u| = 8e-8, sits above rtol 1e-8 (device and oracle both stagnate at
+# 3e-8..1e-5 while restarting, tests/diagnostics/true_residual_gap.py): the case
+# runs at rtol 1e-6, where both meet the reference's true-residual contract.
+@pytest.mark.parametrize("dims,n_geo,kind,rtol", [((16, 8, 8), 1, "weighted_jacobi", 1e-8),
+                                                  ((16, 8, 8), 1, "chebyshev", 1e-8),
+                                                  ((32, 16), 2, "weighted_jacobi", 1e-6),
+                                                  ((24, 12, 12), 2, "chebyshev", 1e-8)])
+def test_hybrid_matches_oracle(dims, n_geo, kind, rtol):
     mesh, g, bc, rho, E, K, Kref = cantilever(dims, 6, void=True)
     w = 1.0 if kind == "chebyshev" else 0.6
     B = T.rigid_body_modes(mesh, bc.fixed_dofs)
@@ -116,10 +118,11 @@ def test_hybrid_matches_oracle(dims, n_geo, kind):
         assert spdiff(h.level_matrix(k), lv.A) <= 1e-11, k
     b = np.random.default_rng(3).standard_normal(g.n_dofs)
     assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-9
-    u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
-    uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
-    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
-    assert rec.converged and abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
+    u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=rtol, max_iterations=3000))
+    uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=rtol, max_iterations=3000)
+    assert rec.converged
+    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, rtol=rtol, maxit=3000))
 
 
 def test_hybrid_full_geo_equals_gmg_and_zero_is_amg():

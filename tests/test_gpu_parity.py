@@ -19,62 +19,49 @@ import paper_2001_01655_b200 as T  # noqa: E402
 from paper_2001_01655_b200 import problems  # noqa: E402
 
 
-class _Transposed:
-    """K^T @ x: the same operator with a different fp64 summation order."""
-
-    def __init__(self, K):
-        self.KT = K.T.tocsr()
-        self.shape = K.shape
-
-    def __matmul__(self, x):
-        return self.KT @ x
-
-
-def _pcg_dots(A, b, M, rtol, maxit, dot):
-    """The oracle's PCG (O.pcg) with a different (equally valid) summation order
-    of its dot products."""
-    x = np.zeros_like(b)
-    r = b - A @ x
-    tol = rtol * np.sqrt(dot(b, b))
-    it = 0
-    if np.sqrt(dot(r, r)) <= tol:
-        return x, it
-    z = M(r)
-    p = z.copy()
-    rz = dot(r, z)
-    for it in range(1, maxit + 1):
-        q = A @ p
-        alpha = rz / dot(p, q)
-        x = x + alpha * p
-        r = r - alpha * q
-        if np.sqrt(dot(r, r)) <= tol:
-            break
-        z = M(r)
-        rz_new = dot(r, z)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-    return x, it
-
+from ckpt_common import Transposed as _Transposed  # noqa: E402
+from ckpt_common import block_dot  # noqa: E402
 
 _DOT_ORDERS = (
-    lambda x, y: float(sum(np.add.reduce(c) for c in np.array_split(x * y, 296))),  # GPU-like block partials
-    lambda x, y: float(np.sum((x * y)[::-1])),                                       # reversed
+    block_dot,                                               # GPU-like block partials
+    lambda x, y: float(np.sum((x * y)[::-1])),               # reversed
 )
 
 
 def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
     """How far the oracle moves from itself when only the summation order
     changes: of the matvec (K^T @ x) and of the dot products (block-partial
-    sums as on the GPU, reversed).  E.g. the 3D SA case (12,6,6) of
-    test_gpu_amg: the oracle takes 54 iterations, 58 with reversed dots.  For strongly ill-conditioned systems (E contrast 1e9)
-    this exceeds the north-star tolerances, which are then unattainable by ANY
-    implementation; tests use max(tolerance, 10 x floor) and say so."""
+    sums as on the GPU, reversed) -- O.pcg under the same true-residual
+    contract.  E.g. the 3D SA case (12,6,6) of test_gpu_amg: the oracle takes
+    54 iterations, 58 with reversed dots.  For strongly ill-conditioned systems
+    (E contrast 1e9) this exceeds the north-star tolerances, which are then
+    unattainable by ANY implementation; tests use max(tolerance, 10 x floor)
+    and say so."""
     u1, r1 = O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit)
-    u2, r2 = O.pcg(_Transposed(Kref), f, None, M, rtol=rtol, max_iterations=maxit)
-    runs = [(u2, r2.iterations)] + [_pcg_dots(Kref, f, M, rtol, maxit, d) for d in _DOT_ORDERS]
+    runs = [O.pcg(_Transposed(Kref), f, None, M, rtol=rtol, max_iterations=maxit)]
+    runs += [O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit, dot=d) for d in _DOT_ORDERS]
     fu = max(rel(u, u1) for u, _ in runs)
     fc = max(abs(f @ u - f @ u1) for u, _ in runs) / abs(f @ u1)
-    return fu, fc, max(abs(r1.iterations - it) for _, it in runs)
+    return fu, fc, max(abs(r1.iterations - r.iterations) for _, r in runs)
+
+
+def assert_pcg_parity(rec, u, reco, uo, f, floor):
+    """Device PCG vs oracle PCG on the same hierarchy, under the reference's
+    true-residual contract (krylov.py:128-129): the same verdict; iterations
+    +-1 (widened to the oracle's own summation-order spread) when converged;
+    when neither converges (E contrast 5e8: the true residual's fp64 floor
+    sits above rtol, both restart from it until the cap) the same cap;
+    u and f.u to max(north star, 10 x floor)."""
+    fu, fc, fi = floor
+    assert rec.converged == reco.converged, (rec.converged, reco.converged, rec.residual_history[-1],
+                                              reco.residual_history[-1])
+    if reco.converged:
+        assert abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi), (rec.iterations, reco.iterations)
+    else:  # both stop at the cap, the true residual above rtol (restart cycles on its fp64 floor)
+        assert rec.iterations == reco.iterations
+    assert rel(u, uo) <= max(1e-8, 10 * fu), (rel(u, uo), fu)
+    c, co = float(f @ u), float(f @ uo)
+    assert abs(c - co) <= max(1e-10, 10 * fc) * abs(co), (abs(c - co) / abs(co), fc)
 
 
 def iteration_tolerance(floor_it):
@@ -188,12 +175,7 @@ def test_pcg_matches_oracle(dims, levels, kind, void):
     cfg = T.SolveConfig(rtol=1e-8, max_iterations=2000)
     u, rec = T.cg_solve(K, bc.load_vector, None, h, cfg)
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=2000)
-    assert rec.converged and reco.converged
-    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply)
-    assert abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
-    assert rel(host(u), uo) <= max(1e-8, 10 * fu)
-    c, co = float(bc.load_vector @ host(u)), float(bc.load_vector @ uo)
-    assert abs(c - co) <= max(1e-10, 10 * fc) * abs(co), (abs(c - co) / abs(co), fc)
+    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector, reproducibility_floor(Kref, bc.load_vector, ho.apply))
     hist = np.array(rec.residual_history)
     n = min(len(hist), len(reco.residual_history), 10)
     assert np.allclose(hist[:n], reco.residual_history[:n], rtol=1e-8)
@@ -209,9 +191,8 @@ def test_jacobi_safeguard_matches_oracle():
     assert rel(host(h.apply(b)), ho.apply(b)) <= 1e-10
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
-    fu, fc, fi = reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000)
-    assert rec.converged and abs(rec.iterations - reco.iterations) <= iteration_tolerance(fi)
-    assert rel(host(u), uo) <= max(1e-8, 10 * fu)
+    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000))
 
 
 def test_pcg_warm_start_and_unpreconditioned():
