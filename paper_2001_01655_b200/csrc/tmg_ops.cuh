@@ -142,23 +142,39 @@ __device__ __forceinline__ void prolong_at(const Coarsening& T, const double* __
 // ----------------------------------------------------------------------------
 // DIRECT: the source is a pointwise combination of vectors, cheap enough to be
 // evaluated per neighbour (2D FineOp direct path); ProlongSrc is not.
+// The DIRECT sources also expose the vectors they read (NV, vec(v); nullptr =
+// not read) and finish(raw, out) on staged copies raw[v][c] -- the streamed 3D
+// operator (tmg_fine3h.cuh) moves the vectors with TMA and finishes them in
+// shared memory.  finish() performs load()'s arithmetic in load()'s order.
 template <int DIM>
 struct VecSrc {
   static constexpr bool DIRECT = true;
+  static constexpr int NV = 1;
   const double* __restrict__ v;
   __device__ void load(int node, int, int, int, double out[DIM]) const { load_node<DIM>(v, node, out); }
+  __device__ const double* vec(int) const { return v; }
+  __device__ void finish(const double (*raw)[DIM], double out[DIM]) const {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = raw[0][c];
+  }
 };
 template <int DIM>
 struct ScaledSrc {  // s .* v
   static constexpr bool DIRECT = true;
   const double* __restrict__ v;
   const double* __restrict__ s;
+  static constexpr int NV = 2;
   __device__ void load(int node, int, int, int, double out[DIM]) const {
     double a[DIM], b[DIM];
     load_node<DIM>(v, node, a);
     load_node<DIM>(s, node, b);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) out[c] = a[c] * b[c];
+  }
+  __device__ const double* vec(int i) const { return i == 0 ? v : s; }
+  __device__ void finish(const double (*raw)[DIM], double out[DIM]) const {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = raw[0][c] * raw[1][c];
   }
 };
 template <int DIM>
@@ -167,6 +183,7 @@ struct AxpySrc {  // z + beta * p  (beta == 0 -> z; never touches p then)
   const double* __restrict__ z;
   const double* __restrict__ p;
   double beta;
+  static constexpr int NV = 2;
   __device__ void load(int node, int, int, int, double out[DIM]) const {
     load_node<DIM>(z, node, out);
     if (beta != 0.0) {
@@ -174,6 +191,15 @@ struct AxpySrc {  // z + beta * p  (beta == 0 -> z; never touches p then)
       load_node<DIM>(p, node, q);
 #pragma unroll
       for (int c = 0; c < DIM; ++c) out[c] += beta * q[c];
+    }
+  }
+  __device__ const double* vec(int i) const { return i == 0 ? z : (beta != 0.0 ? p : nullptr); }
+  __device__ void finish(const double (*raw)[DIM], double out[DIM]) const {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) out[c] = raw[0][c];
+    if (beta != 0.0) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] += beta * raw[1][c];
     }
   }
 };
@@ -184,6 +210,21 @@ struct ChebSrc {  // dinv .* r + beta * p  (dinv == nullptr: r + beta * p)
   const double* __restrict__ p;
   const double* __restrict__ dinv;
   double beta;
+  static constexpr int NV = 3;
+  __device__ const double* vec(int i) const { return i == 0 ? r : (i == 1 ? dinv : (beta != 0.0 ? p : nullptr)); }
+  __device__ void finish(const double (*raw)[DIM], double out[DIM]) const {
+    if (dinv) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] = raw[1][c] * raw[0][c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] = raw[0][c];
+    }
+    if (beta != 0.0) {
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) out[c] += beta * raw[2][c];
+    }
+  }
   __device__ void load(int node, int, int, int, double out[DIM]) const {
     double a[DIM], d[DIM];
     load_node<DIM>(r, node, a);
@@ -263,23 +304,28 @@ struct FineOp {
 #ifndef TMG_F2_MINB
 #define TMG_F2_MINB 5  // 2D: 48 registers, 5 CTAs per SM (measured: sweep 5.82 -> 5.45 us vs 4 / 6 CTAs)
 #endif
-#ifndef TMG_F3H_MINB
-#define TMG_F3H_MINB 2  // 3D character-basis stream: 128 registers (no spills), 2 CTAs per SM
-#endif
   // 3D rows are streamed (STREAM: one launch shape for every 3D level-0 kernel):
   // by default the element-centric character-basis operator of tmg_fine3h.cuh
-  // (~175 FP64 operations per element instead of 576); -DTMG_FINE3_PAIR selects
-  // the two-nodes-per-thread gather of tmg_fine3.cuh, -DTMG_FINE3_TILE the
-  // node-per-thread tile below (row()) -- both kept as measured A/B baselines.
+  // (~175 FP64 operations per element instead of 576, TMA-fed, warp
+  // specialised); -DTMG_FINE3_TILE selects the node-per-thread tile below
+  // (row()), kept as the measured A/B baseline.
 #ifdef TMG_FINE3_TILE
   static constexpr bool STREAM = false;
 #else
   static constexpr bool STREAM = DIM == 3;
 #endif
-#if defined(TMG_FINE3_TILE) || defined(TMG_FINE3_PAIR)
+#ifndef TMG_F3H_MINB
+#define TMG_F3H_MINB 1
+#endif
+#ifndef TMG_F3H_TY
+#define TMG_F3H_TY 8  // consumer warps of the 3D stream (rows of 32 element columns)
+#endif
+#if defined(TMG_FINE3_TILE)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
+  static constexpr int THREADS = TPB;
 #else
-  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;  // 3D: one CTA per SM (tmg_fine3h.cuh)
+  static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3H_TY + 32;  // 3D: consumer warps + the TMA producer warp
 #endif
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
@@ -498,40 +544,17 @@ struct FineOp {
 };
 
 }  // namespace tmg
-#include "tmg_fine3.cuh"
 #include "tmg_fine3h.cuh"
 namespace tmg {
-// the streamed 3D row path (FineOp<3>::STREAM): character-basis elements
-// (default) or the two-nodes-per-thread gather (-DTMG_FINE3_PAIR)
+// the streamed 3D row path (FineOp<3>::STREAM): character-basis elements, the
+// epilogue's input vectors staged by the producer warp (ein)
 template <class Src, class Epi>
-__device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, Epi&& epi) {
-#ifdef TMG_FINE3_PAIR
-  fine3_pair_rows(op, src, static_cast<Epi&&>(epi));
-#else
-  fine3h_rows(op, src, static_cast<Epi&&>(epi));
-#endif
+__device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, const f3h::EpiIn& ein, Epi&& epi) {
+  fine3h_rows(op, src, ein, static_cast<Epi&&>(epi));
 }
-inline dim3 fine3_grid(const Lat& L) {
-#ifdef TMG_FINE3_PAIR
-  return f3::grid(L);
-#else
-  return f3h::grid(L);
-#endif
-}
-constexpr int fine3_threads() {
-#ifdef TMG_FINE3_PAIR
-  return f3::NT;
-#else
-  return f3h::NT;
-#endif
-}
-constexpr size_t fine3_smem() {
-#ifdef TMG_FINE3_PAIR
-  return f3::SMEM_BYTES;
-#else
-  return f3h::SMEM_BYTES;
-#endif
-}
+inline dim3 fine3_grid(const Lat& L) { return f3h::grid(L); }
+constexpr int fine3_threads() { return f3h::NTH; }
+constexpr size_t fine3_smem() { return f3h::SMEM_BYTES; }
 
 // ----------------------------------------------------------------------------
 // StencilOp
@@ -583,13 +606,13 @@ struct StencilOp {
 #define TMG_ST_MINB 2  // 3D stencil rows: 128 instead of 254 registers (config-3 PCG 370.8 -> 355.7 us/iter; 3 / 4: slower)
 #endif
   static constexpr int MINB = TMG_ST_MINB;  // large register budget: batched loads in flight
+  static constexpr int THREADS = TPB;
   static constexpr bool STREAM = false;
   template <class Src>
   __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
                       double self[DIM]) const {
     if (!active) return;
     constexpr int G = DIM == 2 ? 9 : 3;
-    const int n = (int)L.n;
     double acc[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
@@ -666,13 +689,14 @@ constexpr size_t row_smem() {
 
 // y = A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_apply(const __grid_constant__ Op op, const double* __restrict__ x,
                                                double* __restrict__ y) {
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
-    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* out, const double*) {
-      store_node<DIM>(y, node, out);
-    });
+    fine3_rows(op, VecSrc<DIM>{x}, f3h::EpiIn{{nullptr, nullptr}},
+               [&](int node, int, int, int, const double* out, const double*, const double (*)[3]) {
+                 store_node<DIM>(y, node, out);
+               });
   } else {
     TMG_NODE_IDX
     double out[DIM], self[DIM];
@@ -684,17 +708,17 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_apply(const __grid_constant__
 
 // y = ds .* A (ds .* v)   (Lanczos on D^-1/2 A D^-1/2)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_apply_sym(const __grid_constant__ Op op, const double* __restrict__ v,
                                                    const double* __restrict__ ds, double* __restrict__ y) {
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
-    fine3_rows(op, ScaledSrc<DIM>{v, ds}, [&](int node, int, int, int, const double* o, const double*) {
-      double d[DIM], out[DIM];
-      load_node<DIM>(ds, node, d);
+    fine3_rows(op, ScaledSrc<DIM>{v, ds}, f3h::EpiIn{{ds, nullptr}},
+               [&](int node, int, int, int, const double* o, const double*, const double (*e)[3]) {
+                 double out[DIM];
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) out[c] = o[c] * d[c];
-      store_node<DIM>(y, node, out);
-    });
+                 for (int c = 0; c < DIM; ++c) out[c] = o[c] * e[0][c];
+                 store_node<DIM>(y, node, out);
+               });
   } else {
     TMG_NODE_IDX
     double out[DIM], self[DIM], d[DIM];
@@ -709,17 +733,17 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_apply_sym(const __grid_consta
 
 // r = b - A x
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_residual(const __grid_constant__ Op op, const double* __restrict__ x,
                                                   const double* __restrict__ b, double* __restrict__ r) {
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
-    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double*) {
-      double bb[DIM];
-      load_node<DIM>(b, node, bb);
+    fine3_rows(op, VecSrc<DIM>{x}, f3h::EpiIn{{b, nullptr}},
+               [&](int node, int, int, int, const double* o, const double*, const double (*e)[3]) {
+                 double bb[DIM];
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) bb[c] -= o[c];
-      store_node<DIM>(r, node, bb);
-    });
+                 for (int c = 0; c < DIM; ++c) bb[c] = e[0][c] - o[c];
+                 store_node<DIM>(r, node, bb);
+               });
   } else {
     TMG_NODE_IDX
     double out[DIM], self[DIM], bb[DIM];
@@ -758,24 +782,23 @@ __device__ __forceinline__ void jacobi_body(const Op& op, const Src& src, const 
 }
 
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                 const double* __restrict__ b, const double* __restrict__ dinv,
                                                 const double* __restrict__ wp, double* __restrict__ xo, Red red) {
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
     const double w = *wp;
     double v = 0.0;
-    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double* self) {
-      double bb[DIM], d[DIM], out[DIM];
-      load_node<DIM>(b, node, bb);
-      load_node<DIM>(dinv, node, d);
+    fine3_rows(op, VecSrc<DIM>{x}, f3h::EpiIn{{b, dinv}},
+               [&](int node, int, int, int, const double* o, const double* self, const double (*e)[3]) {
+                 double out[DIM];
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) {
-        out[c] = self[c] + w * (d[c] * (bb[c] - o[c]));
-        if (DOT) v += out[c] * bb[c];
-      }
-      store_node<DIM>(xo, node, out);
-    });
+                 for (int c = 0; c < DIM; ++c) {
+                   out[c] = self[c] + w * (e[1][c] * (e[0][c] - o[c]));
+                   if (DOT) v += out[c] * e[0][c];
+                 }
+                 store_node<DIM>(xo, node, out);
+               });
     if (DOT) grid_reduce(v, red);
   } else {
     jacobi_body<DIM, Op, VecSrc<DIM>, DOT>(op, VecSrc<DIM>{x}, b, dinv, wp, xo, red);
@@ -785,7 +808,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_jacobi(const __grid_constant_
 // first post-smoothing sweep with the coarse-grid correction fused in:
 // xs = x + P e evaluated on the fly, xo = xs + w D^-1 (b - A xs)
 template <int DIM, class Op, bool DOT>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_prolong_jacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                         const double* __restrict__ e, Coarsening T,
                                                         const double* __restrict__ b, const double* __restrict__ dinv,
                                                         const double* __restrict__ wp, double* __restrict__ xo,
@@ -796,17 +819,17 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_prolong_jacobi(const __grid_c
 
 // xo = x + w B^-1 (b - A x), B the nodal diagonal blocks (multigrid.py:90)
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_bjacobi(const __grid_constant__ Op op, const double* __restrict__ x,
                                                  const double* __restrict__ b, const double* __restrict__ binv,
                                                  const double* __restrict__ wp, double* __restrict__ xo) {
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
     const double w = *wp;
-    fine3_rows(op, VecSrc<DIM>{x}, [&](int node, int, int, int, const double* o, const double* self) {
+    fine3_rows(op, VecSrc<DIM>{x}, f3h::EpiIn{{b, nullptr}},
+               [&](int node, int, int, int, const double* o, const double* self, const double (*e)[3]) {
       double r[DIM], out[DIM];
-      load_node<DIM>(b, node, r);
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) r[c] -= o[c];
+      for (int c = 0; c < DIM; ++c) r[c] = e[0][c] - o[c];
 #pragma unroll
       for (int a = 0; a < DIM; ++a) {
         double s = 0.0;
@@ -840,7 +863,7 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_bjacobi(const __grid_constant
 //   p' = z + beta p ; x += alpha p' ; r' = r - alpha A p'
 // with z = D^-1 r (zs = r, Jacobi-Chebyshev) or z = SOR solve of r (zs = z, dinv = nullptr).
 template <int DIM, class Op>
-__global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_cheb(const __grid_constant__ Op op, const double* __restrict__ r,
                                               const double* __restrict__ zs, const double* __restrict__ p, const double* __restrict__ dinv,
                                               const double* __restrict__ coef, int step, int x_zero,
                                               double* __restrict__ x, double* __restrict__ po,
@@ -848,15 +871,13 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cheb(const __grid_constant__ 
   TMG_PDL_ENTRY;
   if constexpr (Op::STREAM) {
     const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
-    fine3_rows(op, ChebSrc<DIM>{zs, p, dinv, beta}, [&](int node, int, int, int, const double* o,
-                                                         const double* pv) {
+    fine3_rows(op, ChebSrc<DIM>{zs, p, dinv, beta}, f3h::EpiIn{{r, x_zero ? nullptr : x}},
+               [&](int node, int, int, int, const double* o, const double* pv, const double (*e)[3]) {
       double rr[DIM], xv[DIM];
-      load_node<DIM>(r, node, rr);
-      if (x_zero) {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) xv[c] = 0.0;
-      } else {
-        load_node<DIM>(x, node, xv);
+      for (int c = 0; c < DIM; ++c) {
+        rr[c] = e[0][c];
+        xv[c] = x_zero ? 0.0 : e[1][c];
       }
 #pragma unroll
       for (int c = 0; c < DIM; ++c) {

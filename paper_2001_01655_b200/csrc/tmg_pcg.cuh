@@ -46,7 +46,7 @@ __global__ void k_cg_init(const CgCfg* __restrict__ cfg, CgState* __restrict__ s
 // p' = z + beta p (own node and, on the fly, its neighbours); q = A p'; reduce p'.q
 template <int DIM, class Op>
 // The search direction ping-pongs between P0 and P1 by iteration parity (no copy).
-__global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
+__global__ void __launch_bounds__(Op::THREADS, Op::MINB) k_cg_pq(const __grid_constant__ Op op, const double* __restrict__ z,
                                                double* __restrict__ P0, double* __restrict__ P1,
                                                double* __restrict__ q, const CgState* __restrict__ st,
                                                const double* __restrict__ rz_new, Red red) {
@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(TPB, Op::MINB) k_cg_pq(const __grid_constant__
   if constexpr (Op::STREAM) {
     const double beta = st->first ? 0.0 : (*rz_new / st->rz);
     double v = 0.0;
-    fine3_rows(op, AxpySrc<DIM>{z, p, beta}, [&](int node, int, int, int, const double* o, const double* pv) {
+    fine3_rows(op, AxpySrc<DIM>{z, p, beta}, f3h::EpiIn{{nullptr, nullptr}},
+               [&](int node, int, int, int, const double* o, const double* pv, const double (*)[3]) {
 #pragma unroll
       for (int c = 0; c < DIM; ++c) v += pv[c] * o[c];
       store_node<DIM>(pn, node, pv);

@@ -36,9 +36,12 @@ from oracle import topomg_oracle as O  # noqa: E402
 from paper_2001_01655_b200 import problems as P  # noqa: E402
 
 SCRATCH = os.environ.get("TMG_CKPT_SCRATCH", "/tmp/tmg_ckpt")
-# iteration caps of the fixed-iteration runs (the configs that converge run to
-# convergence under the cap)
-MAXIT = {1: 2000, 2: 3000, 3: 3000, 4: 200}
+# iteration caps of the fixed-iteration runs.  Under the true-residual contract
+# no config reaches rtol 1e-8 (profiles/r02_attainable_accuracy.txt): config 2's
+# recursive residual meets it at ~290 iterations, after which the restarts
+# hover on the true residual's fp64 floor (2e-8..1e-7) -- its cap covers the
+# first restart.
+MAXIT = {1: 2000, 2: 300, 3: 3000, 4: 200}
 JITTER = 1e-14
 
 
@@ -145,8 +148,7 @@ def combine(c):
             out[key + "_perturbed_iterations"] = p["iterations"]
             out[key + "_perturbed_hist"] = p["hist"]
             print(key, "iterations base %d perturbed %d" % (b["iterations"], p["iterations"]),
-                  "floors x", np.array2string(np.array(fx), precision=2), "comp",
-                  np.array2string(np.array(fc), precision=2))
+                  "floors x", " ".join("%.2e" % v for v in fx), "comp", " ".join("%.2e" % v for v in fc))
     path = os.path.join(HERE, "config%d_checkpoints.npz" % c)
     np.savez_compressed(path, **out)
     print("wrote", path)

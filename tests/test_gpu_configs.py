@@ -161,141 +161,112 @@ def test_full_size_preconditioner_is_linear_and_symmetric(c):
         assert abs(a - b) <= 1e-6 * np.linalg.norm(x) * np.linalg.norm(My), leg["strategy"]
 
 
-def test_full_size_config2_four_load_cases_share_one_hierarchy():
-    w, E = workload(2)
-    K = T.assemble_stiffness(w.mesh, w.bc, E)
-    leg = w.solvers[0]
-    h = LegRunner(w, leg).build(K)
-    sols = []
-    for f in [w.bc.load_vector] + list(w.loads):
-        u, rec = T.cg_solve(K, f, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=3000))
-        assert rec.converged
-        r = f - host(K @ u)
-        assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(f)  # true residual (recursive one: 1e-8)
-        sols.append(host(u))
-    assert all(np.isfinite(u).all() for u in sols)
+# ---------------------------------------------------------------------------
+# fixed-iteration parity against the oracle's own full-size runs
+# (tests/golden/make_checkpoints.py -> tests/golden/config{1,2,3,4}_checkpoints.npz)
+# ---------------------------------------------------------------------------
+# None of configs 1-4 meets rtol 1e-8 on the TRUE residual in fp64 (oracle and
+# device alike; profiles/r02_attainable_accuracy.txt: the fp64 rounding floor
+# of the residual of these densities lies above it), so both implementations run
+# to the same iteration cap and the solves are compared where they are well
+# posed: at fixed iteration counts k, the compliance f.x_k (= the energy-norm
+# progress of CG, monotone) and the iterate x_k itself (16 seeded Gaussian
+# projections, tests/ckpt_common.py).  Tolerance per checkpoint:
+# max(north-star tolerance, 10 x the oracle's own floor), the floor being how
+# far the oracle moves from itself under rounding-level changes only (matvec
+# summed transposed, dots in the GPU's block order, 3D SA candidates jittered by
+# 1e-14) -- measured exactly on the full iterates by make_checkpoints.py.
+import ckpt_common as CK  # noqa: E402
+
+CKPT = {}
 
 
-def test_full_size_config1_pcg_trajectories_match_oracle():
-    """The bench workload itself, both legs, 2000 PCG iterations, against the
-    oracle's run on the same input (tests/golden/make_config1_history.py): same
-    hierarchy sizes, the same early residual trajectory, and the same failure
-    mode at the cap (neither reaches rtol 1e-8 on this non-percolating density,
-    DESIGN.md deviation 7).  The early agreement is limited by the coarsest
-    operators (GMG: 2562 dofs, cond 4.6e13), whose direct solves differ in
-    forward error at the percent level between any two implementations
-    (device explicit inverse vs scipy splu, tests/diagnostics/coarse_check.py)."""
+def checkpoints(c):
     import os
-    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "config1_history.npz"))
-    w, E = workload(1)
+    if c not in CKPT:
+        path = os.path.join(os.path.dirname(__file__), "golden", "config%d_checkpoints.npz" % c)
+        if not os.path.exists(path):
+            pytest.skip("config%d_checkpoints.npz not generated" % c)
+        CKPT[c] = dict(np.load(path))
+    return CKPT[c]
+
+
+def leg_key(leg, li):
+    return "%s_l%d" % (P.leg_name(leg).replace("+", "_"), li)
+
+
+def run_checkpoints(c, legs=None):
+    ref = checkpoints(c)
+    w, E = workload(c)
     K = T.assemble_stiffness(w.mesh, w.bc, E)
+    loads = [w.bc.load_vector] + list(w.loads)
+    report = []
     for leg in w.solvers:
-        tag = "gmg" if leg["strategy"] == "gmg" else "amg"
+        if legs and leg["strategy"] not in legs:
+            continue
         h = LegRunner(w, leg).build(K)
-        assert [lv.size for lv in h.levels] == list(ref[tag + "_sizes"]), tag
-        u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=2000))
-        hist = np.array(rec.residual_history)
-        rh = ref[tag + "_hist"]
-        assert len(hist) == len(rh) == 2001, tag
-        d = np.abs(hist - rh) / rh
-        print(tag, "rel. diff of the first 12 residuals", np.array2string(d[:12], precision=3),
-              "final rel. residual gpu %.3e oracle %.3e" % (hist[-1] / hist[0], rh[-1] / rh[0]))
-        assert d[:11].max() <= 0.1, (tag, d[:11])
-        assert not rec.converged and rh[-1] / rh[0] > w.rtol
-        assert 0.1 <= (hist[-1] / hist[0]) / (rh[-1] / rh[0]) <= 10.0, tag
+        for li, f in enumerate(loads):
+            key = leg_key(leg, li)
+            assert [lv.size for lv in h.levels] == list(ref[key + "_sizes"]), key
+            ks, cap = ref[key + "_ks"], int(ref[key + "_iterations"])
+            for n, k in enumerate(list(ks) + [cap]):
+                u, rec = T.cg_solve(K, f, None, h, T.SolveConfig(method="cg", rtol=w.rtol, max_iterations=int(k)))
+                uh = host(u)
+                final = n == len(ks)
+                cr = float(ref[key + "_final_comp"] if final else ref[key + "_comp"][n])
+                pr = ref[key + "_final_proj"] if final else ref[key + "_proj"][n]
+                fl_c = float(ref[key + "_floor_final_comp"] if final else ref[key + "_floor_comp"][n])
+                fl_x = float(ref[key + "_floor_final_x"] if final else ref[key + "_floor_x"][n])
+                dc = abs(float(f @ uh) - cr) / abs(cr)
+                dx = CK.proj_rel(CK.project(uh), pr)
+                report.append((key, int(k), dc, fl_c, dx, fl_x))
+                print("%s k=%5d: compliance rel %.2e (oracle floor %.2e)  x rel %.2e (floor %.2e)  iters %d%s" % (
+                    key, k, dc, fl_c, dx, fl_x, rec.iterations, "  true res %.2e" % (
+                        rec.residual_history[-1] / np.linalg.norm(f))))
+                assert rec.iterations == int(k), (key, k, rec.iterations)
+                assert not rec.converged and not bool(ref[key + "_converged"]) or final
+                assert dc <= max(1e-10, 10 * fl_c), (key, k, dc, fl_c)
+                assert dx <= max(1e-8, 10 * fl_x), (key, k, dx, fl_x)
+            assert rec.converged == bool(ref[key + "_converged"])
+    return report
 
 
-def test_full_size_config2_solves_match_oracle():
-    """BASELINE config 2 at full size (2.46 M dofs, SA-AMG, four load cases on one
-    hierarchy) against the oracle's own solves (tests/golden/make_config2_reference.py):
-    identical hierarchy sizes, converged, iteration counts, compliance and the
-    displacement field through 8 seeded random projections and its norm."""
-    import os
-    path = os.path.join(os.path.dirname(__file__), "golden", "config2_reference.npz")
-    if not os.path.exists(path):
-        pytest.skip("config2_reference.npz not generated")
-    ref = np.load(path)
-    w, E = workload(2)
-    K = T.assemble_stiffness(w.mesh, w.bc, E)
-    h = LegRunner(w, w.solvers[0]).build(K)
-    assert [lv.size for lv in h.levels] == list(ref["sizes"])
-    W = np.random.default_rng(2002).standard_normal((8, w.ndof))
-    for li, f in enumerate([w.bc.load_vector] + list(w.loads)):
-        u, rec = T.cg_solve(K, f, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=3000))
-        uh = host(u)
-        it_ref = len(ref["hist%d" % li]) - 1
-        c, cr = float(f @ uh), float(ref["compliance%d" % li])
-        pr = ref["proj%d" % li]
-        print("load %d: iterations gpu %d oracle %d; compliance rel %.2e; |u| rel %.2e; projections rel %.2e" % (
-            li, rec.iterations, it_ref, abs(c - cr) / abs(cr),
-            abs(np.linalg.norm(uh) - ref["unorm%d" % li]) / ref["unorm%d" % li],
-            np.linalg.norm(W @ uh - pr) / np.linalg.norm(pr)))
-        # measured: identical iteration counts (291/293/282/289), compliance
-        # 6e-12..1.3e-10, projections 7e-9..4e-8 -- both solves stop at rtol 1e-8 on
-        # a cond ~1e12 operator, so the 1e-10 / 1e-8 targets sit at the noise floor
-        assert rec.converged
-        assert abs(rec.iterations - it_ref) <= 1
-        assert abs(c - cr) <= 1e-9 * abs(cr)
-        assert np.linalg.norm(W @ uh - pr) <= 1e-7 * np.linalg.norm(pr)
+def test_full_size_config1_checkpoints_match_oracle():
+    """The bench workload of round 1 (MBB 960x320, GMG-5 and SA-AMG legs on the
+    same input), 2000 PCG iterations: x_k and f.x_k at k = 10, 50, 200, 1000,
+    2000 against the oracle's run."""
+    run_checkpoints(1)
 
 
-def test_full_size_config3_trajectory_matches_oracle():
-    """BASELINE config 3 at full size (698,691 dofs, 3D GMG-4, Jacobi-Chebyshev
-    degree 2 with Lanczos bounds): the oracle's own first 200 PCG iterations
-    (tests/golden/make_config3_history.py) -- same level sizes, same Lanczos
-    bounds, the same residual trajectory."""
-    import os
-    path = os.path.join(os.path.dirname(__file__), "golden", "config3_history.npz")
-    if not os.path.exists(path):
-        pytest.skip("config3_history.npz not generated")
-    ref = np.load(path)
+def test_full_size_config2_checkpoints_match_oracle():
+    """2.46 M dofs, SA-AMG, the four load cases on one hierarchy: k = 10, 50, 200
+    and the 300-iteration cap (the recursive residual meets 1e-8 at ~290, the
+    true one stays on its fp64 floor 2e-8..1e-7, so restarts follow)."""
+    run_checkpoints(2)
+
+
+def test_full_size_config3_checkpoints_match_oracle():
+    """3D GMG-4, Jacobi-Chebyshev: k = 10 .. 3000 against the oracle's 3000-
+    iteration run (its Lanczos bounds to 1e-12)."""
+    ref = checkpoints(3)
     w, E = workload(3)
     K = T.assemble_stiffness(w.mesh, w.bc, E)
     h = LegRunner(w, w.solvers[0]).build(K)
-    assert [lv.size for lv in h.levels] == list(ref["sizes"])
     lm = np.array([h.level_lmax(k) for k in range(h.n_levels - 1)])
-    u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=200))
-    hist, rh = np.array(rec.residual_history), ref["hist"]
-    d = np.abs(hist - rh) / rh
-    print("lmax rel", np.abs(lm - ref["lmax"]) / ref["lmax"], "trajectory rel diff at 10/50/100/200:",
-          [float(d[k]) for k in (10, 50, 100, 200)])
-    assert np.max(np.abs(lm - ref["lmax"]) / ref["lmax"]) <= 1e-10
-    assert len(hist) == len(rh) == 201
-    assert d[:51].max() <= 1e-6  # measured 1e-9 at 10, 1.3e-7 at 50, 2.3e-6 at 200
-    assert d.max() <= 1e-5
+    assert np.max(np.abs(lm - ref["gmg4_l0_lmax"]) / ref["gmg4_l0_lmax"]) <= 1e-12
+    run_checkpoints(3)
 
 
-def test_full_size_config4_trajectory_matches_oracle():
-    """BASELINE config 4 at full size (5,447,811 dofs, hybrid: 3 geometric levels
-    then SA-AMG, Jacobi-Chebyshev everywhere): the oracle's own first 20 PCG
-    iterations (tests/golden/make_config4_history.py) -- same level sizes
-    (geometric and aggregated), same Lanczos bounds, same residual trajectory."""
-    import os
-    path = os.path.join(os.path.dirname(__file__), "golden", "config4_history.npz")
-    if not os.path.exists(path):
-        pytest.skip("config4_history.npz not generated")
-    ref = np.load(path)
+def test_full_size_config4_checkpoints_match_oracle():
+    """The bench workload (3D hybrid, 5.45 M dofs): k = 10, 50, 200.  The first
+    SA level's two-node aggregates carry rank-5 rigid-mode blocks whose trailing
+    Householder column is rounding noise in ANY implementation, so
+    the oracle's own floor here includes 1e-14 jitter of the SA candidates."""
+    ref = checkpoints(4)
     w, E = workload(4)
     K = T.assemble_stiffness(w.mesh, w.bc, E)
     h = LegRunner(w, w.solvers[0]).build(K)
-    assert [lv.size for lv in h.levels] == list(ref["sizes"])
     lm = np.array([h.level_lmax(k) for k in range(h.n_levels - 1)])
-    u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(rtol=w.rtol, max_iterations=20))
-    hist, rh = np.array(rec.residual_history), ref["hist"]
-    d = np.abs(hist - rh) / rh
-    print("lmax rel", np.abs(lm - ref["lmax"]) / ref["lmax"], "trajectory rel diff:", np.array2string(d, precision=2))
-    # The first SA level (407 aggregates on the 12,675-dof operator) has 36
-    # two-node aggregates: two 3-dof nodes carry a rank-5 block of the 6 rigid
-    # modes, so one Householder column of T per such aggregate is rounding noise
-    # in ANY implementation (reference included, DESIGN.md "Case excluded on
-    # purpose"); the operators below it, their Lanczos bound (8.6e-4) and from
-    # iteration 1 the trajectory (0.2-0.5 %, growing to 1-2 % by iteration 20)
-    # differ for that reason alone: the oracle against itself with the SA
-    # candidates perturbed by 1e-14 shows the same (deepest bound 1.2e-3,
-    # trajectory 1-2 %; diagnostics/config4_noise_drift.py).
-    rl = np.abs(lm - ref["lmax"]) / ref["lmax"]
+    rl = np.abs(lm - ref["hybrid3_amg_l0_lmax"]) / ref["hybrid3_amg_l0_lmax"]
     assert rl[:4].max() <= 1e-12  # the geometric levels and the first SA level
-    assert len(hist) == len(rh) == 21
-    assert d[0] <= 1e-12                  # same load vector, same initial residual
-    assert d[:5].max() <= 1e-2
-    assert d.max() <= 5e-2
+    run_checkpoints(4)
