@@ -12,6 +12,11 @@ using namespace tmg;
 struct tmg_operator {
   Operator op;
   std::unique_ptr<PcgCtx> pcg;  // unpreconditioned CG workspace
+  RedSlot sens;                 // compliance reduction of the sensitivity kernel (allocated once)
+  double* comp_host = nullptr;  // pinned landing slot of the compliance scalar
+  ~tmg_operator() {
+    if (comp_host) cudaFreeHost(comp_host);
+  }
 };
 struct tmg_hierarchy {
   std::unique_ptr<Hierarchy> h;
@@ -87,40 +92,93 @@ __global__ void k_check_pos(const double* __restrict__ v, long long n, unsigned*
   if (i < n && !(v[i] > 0.0)) atomicOr(bad, 1u);
 }
 
-// ce_e = u_e^T KE u_e ; optional dc_e = -dE/drho ce_e  (optimization.py:106-129)
+// Per-element strain energy ce_e = u_e^T KE u_e, the sensitivity
+// dc_e = -dE/drho(rho_e) ce_e, and (f != nullptr) the compliance f.u in the
+// same launch (optimization.py:106-111, 124-129).  Grid-stride over elements
+// (x fastest: a warp's corner gathers are contiguous node runs) and over dofs
+// (the compliance dot, reduced deterministically).  3D: the quadratic form in
+// the reflection-character basis of tmg_fine3h.cuh -- u^ = T u_e (a 2x2x2
+// Walsh-Hadamard transform per component) and u_e^T KE u_e = u^T KE^ u^ with
+// the 45-term KE^ (~140 FP64 operations instead of 600).
 template <int DIM>
-__global__ void __launch_bounds__(TPB) k_strain(const __grid_constant__ FineOp<DIM> op, const double* __restrict__ u,
-                                                long long nelem, double* __restrict__ ce,
-                                                const double* __restrict__ rho, double p, double e0, double emin,
-                                                double* __restrict__ dc) {
+__global__ void __launch_bounds__(TPB) k_sens(const __grid_constant__ FineOp<DIM> op, const double* __restrict__ u,
+                                              const double* __restrict__ f, long long nelem, long long ndof,
+                                              double* __restrict__ ce, const double* __restrict__ rho, double p,
+                                              double e0, double emin, double* __restrict__ dc, Red red) {
   TMG_PDL_ENTRY;
   constexpr int NN = 1 << DIM, NE = DIM * NN;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= nelem) return;
-  const int ex = (int)(e % op.ne[0]);
-  const long long t = e / op.ne[0];
-  const int ey = (int)(t % op.ne[1]);
-  const int ez = DIM == 3 ? (int)(t / op.ne[1]) : 0;
-  double ue[NE];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nelem; e += stride) {
+    const int ex = (int)(e % op.ne[0]);
+    const long long t = e / op.ne[0];
+    const int ey = (int)(t % op.ne[1]);
+    const int ez = DIM == 3 ? (int)(t / op.ne[1]) : 0;
+    double s = 0.0;
+    if constexpr (DIM == 3) {
+      double v[8][3];  // corner a = x + 2y + 4z
 #pragma unroll
-  for (int m = 0; m < NN; ++m) {
-    const long long node = op.L.id(ex + corner_x(m), ey + corner_y(m), DIM == 3 ? ez + corner_z(m) : 0);
+      for (int a = 0; a < 8; ++a) {
+        const long long node = op.L.id(ex + (a & 1), ey + ((a >> 1) & 1), ez + (a >> 2));
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) ue[m * DIM + c] = u[node * DIM + c];
+        for (int c = 0; c < 3; ++c) v[a][c] = __ldg(u + node * 3 + c);
+      }
+#pragma unroll
+      for (int b = 1; b < 8; b <<= 1)  // in-place Walsh-Hadamard: v[s] = sum_a (-1)^{popcount(s & a)} v[a]
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+          if (!(a & b))
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const double x0 = v[a][c], x1 = v[a | b][c];
+              v[a][c] = x0 + x1;
+              v[a | b][c] = x0 - x1;
+            }
+#pragma unroll
+      for (int chi = 0; chi < 8; ++chi)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int mi = f3h::blk_member(chi, i);
+          if (mi < 3) continue;  // the mean character: zero row
+          double y = 0.0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const int mj = f3h::blk_member(chi, j);
+            if (f3h::blk_coef(chi, i, j) >= 0) y = fma(op.keh[f3h::blk_coef(chi, i, j)], v[mj / 3][mj % 3], y);
+          }
+          s = fma(v[mi / 3][mi % 3], y, s);
+        }
+    } else {
+      double ue[NE];
+#pragma unroll
+      for (int m = 0; m < NN; ++m) {
+        const long long node = op.L.id(ex + corner_x(m), ey + corner_y(m), 0);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) ue[m * DIM + c] = __ldg(u + node * DIM + c);
+      }
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        double ki = 0.0;
+#pragma unroll
+        for (int j = 0; j < NE; ++j) ki += op.ke[i * NE + j] * ue[j];
+        s += ue[i] * ki;
+      }
+    }
+    if (ce) ce[e] = s;
+    if (dc) {
+      const double r = rho[e];
+      const double dE = p == 1.0 ? (e0 - emin) : p * (e0 - emin) * pow(r, p - 1.0);
+      dc[e] = -dE * s;
+    }
   }
-  double s = 0.0;
-#pragma unroll 4
-  for (int i = 0; i < NE; ++i) {
-    double ki = 0.0;
-#pragma unroll
-    for (int j = 0; j < NE; ++j) ki += op.ke[i * NE + j] * ue[j];
-    s += ue[i] * ki;
-  }
-  if (ce) ce[e] = s;
-  if (dc) {
-    const double r = rho[e];
-    const double dE = p == 1.0 ? (e0 - emin) : p * (e0 - emin) * pow(r, p - 1.0);
-    dc[e] = -dE * s;
+  if (f) {
+    double a = 0.0, b = 0.0;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i + stride < ndof; i += 2 * stride) {
+      a += __ldg(f + i) * __ldg(u + i);
+      b += __ldg(f + i + stride) * __ldg(u + i + stride);
+    }
+    if (i < ndof) a += __ldg(f + i) * __ldg(u + i);
+    grid_reduce(a + b, red);
   }
 }
 
@@ -684,37 +742,42 @@ int tmg_pcg_solve(tmg_operator* K, tmg_hierarchy* h, const double* b, double* x,
   ABI_END
 }
 
-static void launch_strain(const Operator& o, const double* u, double* ce, const double* rho, double p, double e0,
-                          double emin, double* dc, cudaStream_t s) {
-  if (o.dim == 2) {
-    auto f = o.fine<2>();
-    k_strain<2><<<grid_for(o.nelem), TPB, 0, s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
-  } else {
-    auto f = o.fine<3>();
-    k_strain<3><<<grid_for(o.nelem), TPB, 0, s>>>(f, u, o.nelem, ce, rho, p, e0, emin, dc); ::tmg::note_launch();
-  }
+static unsigned sens_grid(long long nelem) { return std::min<unsigned>(grid_for(nelem), RED_BLOCKS * 4u); }
+
+static void launch_sens(tmg_operator& K, const double* u, const double* f, double* ce, const double* rho, double p,
+                        double e0, double emin, double* dc, cudaStream_t s) {
+  const Operator& o = K.op;
+  const unsigned g = sens_grid(o.nelem);
+  if (f && K.sens.part.n < g) K.sens.alloc(g, s);
+  const Red red = f ? K.sens.red() : Red{nullptr, nullptr, nullptr};
+  if (o.dim == 2)
+    launch(k_sens<2>, g, TPB, 0, s, o.fine<2>(), u, f, o.nelem, o.ndof, ce, rho, p, e0, emin, dc, red);
+  else
+    launch(k_sens<3>, g, TPB, 0, s, o.fine<3>(), u, f, o.nelem, o.ndof, ce, rho, p, e0, emin, dc, red);
+  note_launch();
   TMG_CUDA(cudaGetLastError());
 }
 
 int tmg_strain_energy(tmg_operator* K, const double* u, double* ce, void* stream) {
   ABI_BEGIN
   TMG_REQUIRE(K, "operator is NULL");
-  launch_strain(K->op, u, ce, nullptr, 1.0, 1.0, 0.0, nullptr, S(stream));
+  launch_sens(*K, u, nullptr, ce, nullptr, 1.0, 1.0, 0.0, nullptr, S(stream));
   ABI_END
 }
 
+// one launch: dc, and the compliance f.u (landed in pinned memory; the call
+// returns it, so it waits for that one scalar -- no allocation per call)
 int tmg_compliance_sensitivity(tmg_operator* K, const double* rho, const double* f, const double* u, double penalty,
                                double e0, double emin, double* dc, double* compliance, void* stream) {
   ABI_BEGIN
   TMG_REQUIRE(K, "operator is NULL");
   cudaStream_t s = S(stream);
-  launch_strain(K->op, u, nullptr, rho, penalty, e0, emin, dc, s);
+  launch_sens(*K, u, compliance ? f : nullptr, nullptr, rho, penalty, e0, emin, dc, s);
   if (compliance) {
-    RedSlot r;
-    r.alloc(1184, s);
-    k_dot<<<red_grid(K->op.ndof), TPB, 0, s>>>(f, u, K->op.ndof, r.red()); ::tmg::note_launch();
-    TMG_CUDA(cudaMemcpyAsync(compliance, r.res.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (!K->comp_host) TMG_CUDA(cudaMallocHost((void**)&K->comp_host, sizeof(double)));
+    TMG_CUDA(cudaMemcpyAsync(K->comp_host, K->sens.res.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     TMG_CUDA(cudaStreamSynchronize(s));
+    *compliance = *K->comp_host;
   }
   ABI_END
 }

@@ -1,11 +1,14 @@
 // Coarsest-level direct solve (reference: splu of the coarsest operator at build
-// time, multigrid.py:256).  On the B200 the coarse operator is inverted once at
-// setup with a blocked Gauss-Jordan sweep (NB-column pivot blocks, rank-NB
-// trailing updates in register-tiled fp64 tiles), and every V-cycle then applies
-// the explicit inverse as one bandwidth-bound GEMV instead of two latency-bound
-// triangular solves.
+// time, multigrid.py:256).  On the B200 the coarse operator is factorised once
+// at setup -- blocked Cholesky on the FP64 tensor pipe, the explicit inverse
+// formed from the factor (tmg_chol.cuh) -- and every V-cycle then applies the
+// inverse as one bandwidth-bound GEMV instead of two latency-bound triangular
+// solves.  TMG_COARSE=gj selects the blocked Gauss-Jordan inverse below (the
+// round-1 path: NB-column pivot blocks, rank-NB DMMA trailing updates), kept
+// as the measured A/B baseline.
 #pragma once
 #include "tmg_common.cuh"
+#include "tmg_chol.cuh"
 
 namespace tmg {
 
@@ -308,13 +311,27 @@ inline bool dense_mma() {
   return on;
 }
 
-// Dense SPD inverse on the device (setup; stream-ordered, no host sync).
+// Dense SPD inverse on the device (setup; stream-ordered, no host sync): Cholesky
+// (default) or Gauss-Jordan (TMG_COARSE=gj).
 struct DenseInverse {
   long long n = 0;
   DevBuf<double> A;  // holds the inverse after build()
   DevBuf<double> D, RowP, ColP;
   DevBuf<unsigned> bad;
+  static bool use_gj() {
+    static const bool gj = [] {
+      const char* e = std::getenv("TMG_COARSE");
+      return e && e[0] == 'g';
+    }();
+    return gj;
+  }
   void build(cudaStream_t s) {
+    if (!use_gj()) {
+      bad.alloc(1, s);
+      bad.zero(s);
+      cholesky_inverse(A.get(), n, bad.get(), s);
+      return;
+    }
     D.alloc(GJ_NB * GJ_NB, s);
     RowP.alloc((size_t)GJ_NB * n, s);
     ColP.alloc((size_t)GJ_NB * n, s);

@@ -174,13 +174,15 @@ void lvl_sweep(const Hierarchy& H, const Level& l, const double* b, const double
 }
 template <int DIM>
 void lvl_cheb_step(const Level& l, const double* rin, const double* zs, const double* dv, const double* pin, int i,
-                   bool x_zero, double* x, double* po, double* ro, cudaStream_t s) {
+                   bool x_zero, double* x, double* po, double* ro, cudaStream_t s, bool store_p = true) {
   if (l.lattice()) {
-    // ro == nullptr marks the last step of a pass: neither r' nor p' is read
-    // again (lattice rows form p' of their neighbours on the fly)
+    // !store_p / ro == nullptr: p' / r' not stored (the last step of a pass;
+    // r' is kept when the V-cycle reads it as its pre-smoothing residual).
+    // Lattice rows form p' of their neighbours on the fly; the BSR path below
+    // materialises p' (po) first.
     with_lattice<DIM>(l, [&](auto o) {
       launch(k_cheb<DIM, decltype(o)>, TMG_ROW_OP_LAUNCH(l), s, o, rin, zs, pin, dv, l.coef.get(), i, x_zero ? 1 : 0, x,
-                                                           ro ? po : nullptr, ro);
+             store_p ? po : nullptr, ro);
     });
     note_launch();
   } else {
@@ -615,8 +617,15 @@ std::unique_ptr<Hierarchy> build_smoother(const Operator& K, const SmootherCfg& 
 // ----------------------------------------------------------------------------
 
 // Chebyshev passes on x (in place); x_zero: x holds garbage and means 0.
+// `passes` Chebyshev passes on level l, x in/out.  want_r: the last step also
+// stores its maintained residual r' = r - alpha A p' (= b - A x in exact
+// arithmetic) and the buffer holding it is returned, so the V-cycle's residual
+// after pre-smoothing costs no operator application (the reference recomputes
+// b - A x, multigrid.py:238-239; the two differ by fp64 rounding only).
 template <int DIM>
-void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero, int passes, cudaStream_t s) {
+const double* smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero, int passes,
+                          cudaStream_t s, bool want_r = false) {
+  const double* rlast = nullptr;
   for (int p = 0; p < passes; ++p) {
     const double* rin;
     if (x_zero) {
@@ -640,13 +649,18 @@ void smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero
         zs = l.z.get();
         dv = nullptr;
       }
-      // the last step's r' is never read (the next pass starts from b - A x)
-      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, i + 1 < H.sm.degree ? ro : nullptr, s);
+      // the last step's r' is read only by the V-cycle (want_r, last pass); p'
+      // of the last step is never read
+      const bool last = i + 1 == H.sm.degree;
+      const bool keep_r = !last || (want_r && p + 1 == passes);
+      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, keep_r ? ro : nullptr, s, !last);
+      if (last && keep_r) rlast = ro;
       rin = ro;
       pin = po;
     }
     x_zero = false;
   }
+  return rlast;
 }
 
 template <int DIM>
@@ -689,9 +703,14 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
   }
   Level& c = *H.lv[k + 1];
   const bool cheb = cheb_kind(H.sm.kind) || H.sm.kind == SM_SOR_GMRES;  // in-place polynomial / Krylov smoothers
-  auto smooth_poly = [&](double* x, bool x_zero, int passes) {
+  static const bool reuse_r = [] {
+    const char* e = std::getenv("TMG_CHEB_RESIDUAL");
+    return !(e && e[0] == '0');  // 0: recompute b - A x after pre-smoothing (the reference's order of work)
+  }();
+  const double* r_pre = nullptr;
+  auto smooth_poly = [&](double* x, bool x_zero, int passes, bool want_r) {
     if (H.sm.kind == SM_SOR_GMRES) smooth_sor_gmres<DIM>(H, l, b, x, x_zero, passes, s);
-    else smooth_cheb<DIM>(H, l, b, x, x_zero, passes, s);
+    else r_pre = smooth_cheb<DIM>(H, l, b, x, x_zero, passes, s, want_r && reuse_r);
   };
   const int W = H.n_pre + H.n_post;
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? xout : l.xt.get(); };
@@ -700,7 +719,7 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
   int widx = 0;
   if (cheb) {
     if (H.n_pre > 0) {
-      smooth_poly(xout, true, H.n_pre);
+      smooth_poly(xout, true, H.n_pre, true);
       xcur = xout;
     }
   } else {
@@ -711,7 +730,9 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
     }
   }
   const double* r = b;
-  if (xcur) {
+  if (r_pre) {
+    r = r_pre;  // maintained by the last Chebyshev step
+  } else if (xcur) {
     lvl_residual<DIM>(l, xcur, b, l.r.get(), s);
     r = l.r.get();
   }
@@ -734,7 +755,7 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
                             (fuse_mode == 2 || (fuse_mode == 1 && l.opkind == OP_FINE));
   if (!fuse_prolong) xfer_prolong_add<DIM>(H, k, xcur, s);
   if (cheb) {
-    smooth_poly(xcur, false, H.n_post);
+    smooth_poly(xcur, false, H.n_post, false);
   } else {
     for (int p = 0; p < H.n_post; ++p) {
       double* dst = buf(++widx);

@@ -12,8 +12,11 @@ Gaussian vectors; the iterates themselves go to a scratch directory.
 
 `perturbed` is the same oracle with only rounding-level changes: the matvec
 summed in the transposed order (K^T @ x), the dots in the GPU's 296-block
-order, and (SA levels of 3D problems) the rigid-mode candidates jittered by
-1e-14 -- the reproducibility floor of each observable.
+order, the coarsest solve by a different backward-stable factorisation (dense
+Cholesky instead of SuperLU; the coarsest Galerkin operators of these
+densities have cond 1e6..1e14, so ANY two direct solvers differ there by up to
+cond x eps), and (SA levels of 3D problems) the rigid-mode candidates jittered
+by 1e-14 -- the reproducibility floor of each observable.
 
 `combine` writes tests/golden/config{C}_checkpoints.npz: the base run's
 observables, and per checkpoint the EXACT base-vs-perturbed distance of the
@@ -49,7 +52,26 @@ def leg_tag(leg):
     return P.leg_name(leg).replace("+", "_")
 
 
+def other_coarse_solve(h):
+    """Replace the coarsest SuperLU solve by dense Cholesky (LU of the transpose
+    if the matrix is not numerically SPD): an equally backward-stable solver."""
+    import scipy.linalg as sla
+    A = h.levels[-1].A.toarray()
+    try:
+        cf = sla.cho_factor(A)
+        h.coarse_solve = lambda b: sla.cho_solve(cf, b)
+    except np.linalg.LinAlgError:
+        lu = sla.lu_factor(A.T)
+        h.coarse_solve = lambda b: sla.lu_solve(lu, b, trans=1)
+    return h
+
+
 def build(c, w, g, K, leg, perturbed):
+    h = _build(c, w, g, K, leg, perturbed)
+    return other_coarse_solve(h) if perturbed else h
+
+
+def _build(c, w, g, K, leg, perturbed):
     jit = JITTER if (perturbed and len(w.mesh.dims) == 3) else 0.0
     if leg["smoother"] == "chebyshev":
         sm = O.Smoother("chebyshev", 1.0, leg["degree"], lanczos_steps=leg["lanczos_steps"])
