@@ -653,7 +653,18 @@ const double* smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bo
       // of the last step is never read
       const bool last = i + 1 == H.sm.degree;
       const bool keep_r = !last || (want_r && p + 1 == passes);
-      lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, keep_r ? ro : nullptr, s, !last);
+      static const bool x_only = [] {
+        const char* e = std::getenv("TMG_CHEB_XONLY");
+        return !(e && e[0] == '0');  // 0: the full step (operator applied, result dropped) -- A/B
+      }();
+      if (last && !keep_r && x_only) {
+        // neither p' nor r' of this step is read: x += alpha p' needs no operator application
+        launch(k_cheb_x_only, grid_for(l.ndof), TPB, 0, s, zs, pin, dv, (const double*)l.coef.get(), i,
+               (x_zero && i == 0) ? 1 : 0, x, l.ndof);
+        note_launch();
+      } else {
+        lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, keep_r ? ro : nullptr, s, !last);
+      }
       if (last && keep_r) rlast = ro;
       rin = ro;
       pin = po;

@@ -307,7 +307,7 @@ struct FineOp {
   // 3D rows are streamed (STREAM: one launch shape for every 3D level-0 kernel):
   // by default the element-centric character-basis operator of tmg_fine3h.cuh
   // (~175 FP64 operations per element instead of 576, TMA-fed, warp
-  // specialised); -DTMG_FINE3_TILE selects the node-per-thread tile below
+  // specialised); -DTMG_F3S selects the register-prefetch variant of tmg_fine3s.cuh (measured slower), -DTMG_FINE3_TILE the node-per-thread tile below
   // (row()), kept as the measured A/B baseline.
 #ifdef TMG_FINE3_TILE
   static constexpr bool STREAM = false;
@@ -323,9 +323,18 @@ struct FineOp {
 #if defined(TMG_FINE3_TILE)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
   static constexpr int THREADS = TPB;
-#else
+#elif !defined(TMG_F3S)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;  // 3D: one CTA per SM (tmg_fine3h.cuh)
   static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3H_TY + 32;  // 3D: consumer warps + the TMA producer warp
+#else
+#ifndef TMG_F3S_TY
+#define TMG_F3S_TY 8
+#endif
+#ifndef TMG_F3S_MINB
+#define TMG_F3S_MINB 2
+#endif
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3S_MINB;  // 3D: tmg_fine3s.cuh
+  static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3S_TY;
 #endif
 
   // out = (Z K Z + I_fixed) row block of node (i,j,k) applied to src.  Called by
@@ -545,16 +554,27 @@ struct FineOp {
 
 }  // namespace tmg
 #include "tmg_fine3h.cuh"
+#include "tmg_fine3s.cuh"
 namespace tmg {
 // the streamed 3D row path (FineOp<3>::STREAM): character-basis elements, the
 // epilogue's input vectors staged by the producer warp (ein)
 template <class Src, class Epi>
 __device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, const f3h::EpiIn& ein, Epi&& epi) {
+#ifndef TMG_F3S
   fine3h_rows(op, src, ein, static_cast<Epi&&>(epi));
+#else
+  fine3s_rows(op, src, ein, static_cast<Epi&&>(epi));
+#endif
 }
+#ifndef TMG_F3S
 inline dim3 fine3_grid(const Lat& L) { return f3h::grid(L); }
 constexpr int fine3_threads() { return f3h::NTH; }
 constexpr size_t fine3_smem() { return f3h::SMEM_BYTES; }
+#else
+inline dim3 fine3_grid(const Lat& L) { return f3s::grid(L); }
+constexpr int fine3_threads() { return f3s::NT; }
+constexpr size_t fine3_smem() { return f3s::SMEM_BYTES; }
+#endif
 
 // ----------------------------------------------------------------------------
 // StencilOp

@@ -34,12 +34,19 @@ def block_dot(x, y, nblk=296):
     return float(sum(np.add.reduce(c) for c in np.array_split(x * y, nblk)))
 
 
-class Transposed:
-    """K^T @ x: the same (symmetric) operator with another fp64 summation order."""
+class Reordered:
+    """K @ x with every row summed in the REVERSE column order (the columns of K
+    and the entries of x reversed, indices re-sorted): the same operator at
+    another fp64 summation order.  (K^T @ x would not do: K is exactly symmetric,
+    so CSR rows of K^T hold the same entries in the same order.)"""
 
     def __init__(self, K):
-        self.KT = K.T.tocsr()
+        import scipy.sparse as sp
+        K = sp.csr_matrix(K)
+        n = K.shape[1]
+        self.Kr = sp.csr_matrix((K.data.copy(), n - 1 - K.indices, K.indptr.copy()), shape=K.shape)
+        self.Kr.sort_indices()
         self.shape = K.shape
 
     def __matmul__(self, x):
-        return self.KT @ x
+        return self.Kr @ np.ascontiguousarray(x[::-1])

@@ -11,12 +11,19 @@ the checkpoints k of tests/ckpt_common.CHECKPOINTS the compliance f.x_k,
 Gaussian vectors; the iterates themselves go to a scratch directory.
 
 `perturbed` is the same oracle with only rounding-level changes: the matvec
-summed in the transposed order (K^T @ x), the dots in the GPU's 296-block
-order, the coarsest solve by a different backward-stable factorisation (dense
+summed in the reverse column order (ckpt_common.Reordered), the Galerkin
+products associated as P^T (A P) instead of (P^T A) P, the dots in the GPU's
+296-block order, the element matrix KE perturbed in its last bit (the
+reference forms it with BLAS matmuls, mesh.py:254-267, so its last bits are
+implementation-defined; they decide the residual "ghost force" K u of a rigid
+translation u of a floating solid island, which is what the near-singular
+modes of these densities see), the coarsest solve by a different backward-stable factorisation (dense
 Cholesky instead of SuperLU; the coarsest Galerkin operators of these
 densities have cond 1e6..1e14, so ANY two direct solvers differ there by up to
-cond x eps), and (SA levels of 3D problems) the rigid-mode candidates jittered
-by 1e-14 -- the reproducibility floor of each observable.
+cond x eps), and (SA levels) the rigid-mode candidates jittered
+by 1e-14 (aggregates with rank-deficient candidate blocks get a rounding-noise
+Householder column in ANY implementation) -- the reproducibility floor of each
+observable.
 
 `combine` writes tests/golden/config{C}_checkpoints.npz: the base run's
 observables, and per checkpoint the EXACT base-vs-perturbed distance of the
@@ -66,13 +73,35 @@ def other_coarse_solve(h):
     return h
 
 
+def last_bit_jitter(ke, seed=11):
+    """KE with every entry moved by at most one unit in the last place, kept
+    exactly symmetric."""
+    r = np.random.default_rng(seed).uniform(-1.0, 1.0, ke.shape)
+    r = np.triu(r) + np.triu(r, 1).T
+    return ke * (1.0 + np.finfo(float).eps * r)
+
+
+def galerkin_right_first(A, P):
+    """oracle.galerkin with the other association: P^T (A P)."""
+    Ac = (P.T @ (A @ P)).tocsr()
+    Ac.sum_duplicates()
+    return Ac
+
+
 def build(c, w, g, K, leg, perturbed):
-    h = _build(c, w, g, K, leg, perturbed)
-    return other_coarse_solve(h) if perturbed else h
+    if not perturbed:
+        return _build(c, w, g, K, leg, False)
+    keep = O.galerkin
+    O.galerkin = galerkin_right_first
+    try:
+        h = _build(c, w, g, K, leg, True)
+    finally:
+        O.galerkin = keep
+    return other_coarse_solve(h)
 
 
 def _build(c, w, g, K, leg, perturbed):
-    jit = JITTER if (perturbed and len(w.mesh.dims) == 3) else 0.0
+    jit = JITTER if perturbed else 0.0
     if leg["smoother"] == "chebyshev":
         sm = O.Smoother("chebyshev", 1.0, leg["degree"], lanczos_steps=leg["lanczos_steps"])
     else:
@@ -100,8 +129,16 @@ def run(c, variant, maxit):
     w = P.CONFIGS[c]()
     g = O.make_grid(w.mesh.dims)
     E = O.simp_modulus(w.rho, P.PENAL, P.E0, P.EMIN)
-    K = O.assemble_stiffness(g, w.bc.fixed_dofs, E)
-    A = CK.Transposed(K) if perturbed else K
+    if perturbed:
+        keep = O.element_stiffness
+        O.element_stiffness = lambda *a, **k: last_bit_jitter(keep(*a, **k))
+        try:
+            K = O.assemble_stiffness(g, w.bc.fixed_dofs, E)
+        finally:
+            O.element_stiffness = keep
+    else:
+        K = O.assemble_stiffness(g, w.bc.fixed_dofs, E)
+    A = CK.Reordered(K) if perturbed else K
     dot = CK.block_dot if perturbed else None
     print("config %d %s: assembly %.1f s" % (c, variant, time.time() - t0), flush=True)
     loads = [w.bc.load_vector] + list(w.loads)

@@ -19,7 +19,7 @@ import paper_2001_01655_b200 as T  # noqa: E402
 from paper_2001_01655_b200 import problems  # noqa: E402
 
 
-from ckpt_common import Transposed as _Transposed  # noqa: E402
+from ckpt_common import Reordered as _Reordered  # noqa: E402
 from ckpt_common import block_dot  # noqa: E402
 
 _DOT_ORDERS = (
@@ -30,7 +30,7 @@ _DOT_ORDERS = (
 
 def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
     """How far the oracle moves from itself when only the summation order
-    changes: of the matvec (K^T @ x) and of the dot products (block-partial
+    changes: of the matvec (rows summed in reverse column order) and of the dot products (block-partial
     sums as on the GPU, reversed) -- O.pcg under the same true-residual
     contract.  E.g. the 3D SA case (12,6,6) of test_gpu_amg: the oracle takes
     54 iterations, 58 with reversed dots.  For strongly ill-conditioned systems
@@ -38,7 +38,7 @@ def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
     unattainable by ANY implementation; tests use max(tolerance, 10 x floor)
     and say so."""
     u1, r1 = O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit)
-    runs = [O.pcg(_Transposed(Kref), f, None, M, rtol=rtol, max_iterations=maxit)]
+    runs = [O.pcg(_Reordered(Kref), f, None, M, rtol=rtol, max_iterations=maxit)]
     runs += [O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit, dot=d) for d in _DOT_ORDERS]
     fu = max(rel(u, u1) for u, _ in runs)
     fc = max(abs(f @ u - f @ u1) for u, _ in runs) / abs(f @ u1)
