@@ -353,13 +353,14 @@ def run_b200(args, rank, world, local):
     launches = L.tmg_launch_count() - launches0
     total_ms, value = replica_throughput(total_ms, total_work, world, "cuda")
     roof = roofline(args, w, state, L)
+    sens = sensitivity_roofline(args, w, K, L, law, rho_d, f_d, dc, roof["peak"])
     e2e = e2e_run(args, w, K, hs, L, law, world)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "setup_ms": setup_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config %d)" % args.config,
             "config": config_dict(w, args, world), "leg_results": state["legs"],
-            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+            "roofline": roof, "sensitivity": sens, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ol = OracleLegs(w, threads=1)
         wk, dt = ol.step(1)
@@ -416,6 +417,28 @@ def roofline(args, w, state, L):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
             "timing": "CUDA events around one replay of a CUDA graph of %d back-to-back launches" % args.roofline_reps,
             "note": "working set %.0f MB vs 126 MB L2" % (bytes_launch / 1e6)}
+
+
+def sensitivity_roofline(args, w, K, L, law, rho_d, f_d, dc, peak):
+    """The fused compliance + sensitivity kernel k_sens (optimization.py:106-111,
+    124-129): per launch it reads u and f (8 B per dof each), rho (8 B per
+    element) and writes dc (8 B per element).  Timed as a CUDA graph of
+    back-to-back launches rotating over three copies of u and f (HBM-fed)."""
+    import torch
+    from paper_2001_01655_b200._dev import as_dev, ptr
+    from paper_2001_01655_b200._lib import check
+    u = as_dev(np.random.default_rng(3).standard_normal(w.ndof))
+    ms = C.c_double()
+    reps = 3 * max(1, args.roofline_reps // 3)
+    check(L.tmg_operator_time_sensitivity(K.handle, ptr(rho_d), ptr(f_d), ptr(u), law.penalty, law.e_max, law.e_min,
+                                          ptr(dc), reps, C.byref(ms), torch.cuda.current_stream().cuda_stream))
+    nbytes = 16 * w.ndof + 16 * w.mesh.element_count
+    achieved = nbytes / (ms.value / 1e3) / 1e9
+    return {"kernel": "k_sens<%d> (compliance f.u + per-element dc in one launch)" % w.mesh.ndim, "bound": "hbm",
+            "launch_us": ms.value * 1e3, "bytes_per_launch": int(nbytes), "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak,
+            "timing": "CUDA events around one replay of a CUDA graph of %d back-to-back launches rotating over 3 "
+                      "copies of u and f" % reps}
 
 
 def e2e_run(args, w, K, hs, L, law, world=1):

@@ -228,6 +228,13 @@ int tmg_strain_energy(tmg_operator* K, const double* u_dev, double* ce_dev, void
 int tmg_compliance_sensitivity(tmg_operator* K, const double* rho_dev, const double* f_dev,
                                const double* u_dev, double penalty, double e0, double emin,
                                double* dc_dev, double* compliance_host, void* stream);
+/* Average device time (ms) of the fused compliance + sensitivity kernel: `reps`
+ * launches in one CUDA graph, rotating over three copies of u and f so that they
+ * stream from HBM (bench.py's `sensitivity` entry; a measurement helper like
+ * tmg_hierarchy_time_smoother, it replaces no reference function). */
+int tmg_operator_time_sensitivity(tmg_operator* K, const double* rho_dev, const double* f_dev,
+                                  const double* u_dev, double penalty, double e0, double emin,
+                                  double* dc_dev, int32_t reps, double* ms_host, void* stream);
 
 /* End-to-end drop-in for compliance_and_sensitivity (optimization.py:114) given the
  * filtered densities: HOST buffers in and out; H2D copies, modulus, operator,

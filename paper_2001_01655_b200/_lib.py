@@ -93,6 +93,8 @@ _SIGS = {
     "tmg_strain_energy": (C.c_int, [_P, _P, _P, _P]),
     "tmg_compliance_sensitivity": (C.c_int, [_P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
                                              _P, _D, _P]),
+    "tmg_operator_time_sensitivity": (C.c_int, [_P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
+                                                _P, C.c_int32, _D, _P]),
     "tmg_solve_compliance_host": (C.c_int, [C.POINTER(MeshDesc), _P, _P, C.c_int64, _P, C.c_double,
                                             C.c_double, C.c_double, C.c_double, C.POINTER(MgDesc),
                                             C.POINTER(SolveDesc), _P, _P, _D, C.POINTER(SolveRec)]),

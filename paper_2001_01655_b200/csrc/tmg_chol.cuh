@@ -33,13 +33,29 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // operand below it is known to vanish (triangular factors).
 // Fragments (PTX m8n8k4 .f64 row.col): lane l = 4g + t holds A[g][t], B[t][g]
 // and C[g][2t..2t+1] of its 8x8 tile; warp w owns a 16 x 32 sub-tile.
+// Batched (blockIdx.z = q): operands advance by sA / sB / sC doubles per batch
+// entry and entry q has Mq = min(M, Mtot - q * dM) rows (dM = 0: every entry M).
+struct GemmBatch {
+  long long sA = 0, sB = 0, sC = 0;
+  int Mtot = 0, dM = 0;
+  int k_is_m = 0;  // 1: the contraction length of entry q is Mq too (A operand Mq x Mq)
+};
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) k_dgemm_tile(int M, int N, int K, double alpha, const double* __restrict__ A,
                                                     long long lda, const double* __restrict__ B, long long ldb,
                                                     double beta, double* __restrict__ C, long long ldc, int lower,
-                                                    int kmin) {
+                                                    int kmin, GemmBatch bt) {
   TMG_PDL_ENTRY;
   if (lower && blockIdx.y < blockIdx.x) return;
+  if (gridDim.z > 1 || bt.dM) {
+    const long long q = blockIdx.z;
+    A += q * bt.sA;
+    B += q * bt.sB;
+    C += q * bt.sC;
+    if (bt.dM) M = min(M, bt.Mtot - (int)q * bt.dM);
+    if (bt.k_is_m) K = M;
+    if ((int)(blockIdx.y * GT_M) >= M) return;  // (whole CTA)
+  }
   __shared__ double As[GT_K][GT_M + 4];  // As[kk][ii] = op(A)[i0+ii][k0+kk]
   __shared__ double Bs[GT_K][GT_M + 4];  // Bs[kk][jj] = op(B)[k0+kk][j0+jj]
   const int i0 = blockIdx.y * GT_M, j0 = blockIdx.x * GT_M;
@@ -94,10 +110,15 @@ __global__ void __launch_bounds__(256) k_dgemm_tile(int M, int N, int K, double 
   }
 }
 
-// Diagonal block k0 (kb <= CH_NB): L11 = chol(A11) in shared memory, written
-// back into A's lower triangle, and Dinv = L11^-1 (lower) for the panel solve
-// and the block rows of L^-1.  One CTA of 256 threads.
-__global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, long long n, int k0, int kb,
+// Diagonal block k0 (kb <= CH_NB): L11 = chol(A11), written back into A's lower
+// triangle, and Dinv = L11^-1 (lower) for the panel solve and the inverse.  One
+// CTA of 1024 threads (16 per row), ONE barrier per elimination step: step p reads the pivot d = S[p][p] and
+// the still unscaled column p, updates the trailing lower triangle with
+// S[i][j] -= S[i][p] S[j][p] / d (the scaling by sqrt(d) is applied to all columns
+// at the end: L[i][p] = S[i][p] / sqrt(d_p)) and eliminates column p from the
+// rows below it in Y (Y starts as the identity and ends as the inverse of the
+// unit-lower factor, rescaled at the end as well).
+__global__ void __launch_bounds__(1024) k_chol_diag(double* __restrict__ A, long long n, int k0, int kb,
                                                    double* __restrict__ Dinv, unsigned* __restrict__ bad) {
   TMG_PDL_ENTRY;
   extern __shared__ double chol_sm[];  // S[CH_NB][CH_NB + 1], Y[CH_NB][CH_NB + 1]
@@ -107,40 +128,30 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, long 
   for (int q = t; q < kb * kb; q += blockDim.x) {
     const int i = q / kb, j = q % kb;
     S[i][j] = i >= j ? A[(long long)(k0 + i) * n + k0 + j] : 0.0;
+    Y[i][j] = i == j ? 1.0 : 0.0;
   }
-  __syncthreads();
-  // right-looking unblocked Cholesky of the lower triangle
+  // thread -> (row i, column group): 16 threads per row, columns j = g, g + 16, ...
+  const int ri = t >> 4, g = t & 15;
   for (int p = 0; p < kb; ++p) {
-    if (t == 0) {
-      const double d = S[p][p];
-      if (!(d > 0.0)) atomicOr(bad, 1u);
-      S[p][p] = d > 0.0 ? sqrt(d) : 1.0;
-    }
     __syncthreads();
-    const double lpp = S[p][p];
-    for (int i = p + 1 + t; i < kb; i += blockDim.x) S[i][p] /= lpp;
-    __syncthreads();
-    const int m = kb - p - 1;
-    for (int q = t; q < m * m; q += blockDim.x) {
-      const int i = p + 1 + q / m, j = p + 1 + q % m;
-      if (j <= i) S[i][j] -= S[i][p] * S[j][p];
-    }
-    __syncthreads();
-  }
-  // Y = L11^-1 by forward substitution, one column of Y per thread
-  for (int j = t; j < kb; j += blockDim.x) {
-    for (int i = 0; i < kb; ++i) {
-      if (i < j) { Y[i][j] = 0.0; continue; }
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int q = j; q < i; ++q) s -= S[i][q] * Y[q][j];
-      Y[i][j] = s / S[i][i];
+    const double d = S[p][p];
+    if (t == 0 && !(d > 0.0)) atomicOr(bad, 1u);
+    if (ri > p && ri < kb) {
+      const double m = S[ri][p] / (d > 0.0 ? d : 1.0);  // multiplier of row p for row ri (unit-lower L)
+      for (int j = p + 1 + g; j <= ri; j += 16) S[ri][j] -= m * S[j][p];
+      // unit-lower inverse: Yrow_ri -= m * Yrow_p (columns <= p are the nonzeros of row p)
+      for (int j = g; j <= p; j += 16) Y[ri][j] -= m * Y[p][j];
     }
   }
   __syncthreads();
+  // A11 = Lu D Lu^T (Lu unit lower = S[i][j] / S[j][j], D = pivots) -> L = Lu sqrt(D),
+  // L^-1 = sqrt(D)^-1 Lu^-1
   for (int q = t; q < kb * kb; q += blockDim.x) {
     const int i = q / kb, j = q % kb;
-    if (i >= j) A[(long long)(k0 + i) * n + k0 + j] = S[i][j];
-    Dinv[(long long)i * CH_NB + j] = Y[i][j];
+    const double dj = S[j][j] > 0.0 ? S[j][j] : 1.0, di = S[i][i] > 0.0 ? S[i][i] : 1.0;
+    if (i > j) A[(long long)(k0 + i) * n + k0 + j] = S[i][j] / sqrt(dj);
+    else if (i == j) A[(long long)(k0 + i) * n + k0 + j] = sqrt(dj);
+    Dinv[(long long)i * CH_NB + j] = i >= j ? Y[i][j] / sqrt(di) : 0.0;
   }
 }
 
@@ -174,43 +185,61 @@ inline void cholesky_inverse(double* a, long long n, unsigned* bad, cudaStream_t
   DevBuf<double> Dinv, Y, P;
   Dinv.alloc((size_t)nb * CH_NB * CH_NB, s);
   Y.alloc((size_t)n * n, s);
-  P.alloc((size_t)n * CH_NB, s);  // panel / block-row scratch
+  P.alloc((size_t)n * n, s);  // panel scratch (factor), T = L_BA Y_AA (inverse)
+  const GemmBatch one{};
   // 1. A = L L^T (L in A's lower triangle); Dinv_k = L_kk^-1
   for (int k = 0; k < nb; ++k) {
     const int k0 = k * CH_NB, kb = (int)std::min<long long>(CH_NB, n - k0), k1 = k0 + kb;
     double* Dk = Dinv.get() + (size_t)k * CH_NB * CH_NB;
-    launch(k_chol_diag, 1, 256, 2 * CH_NB * (CH_NB + 1) * sizeof(double), s, a, n, k0, kb, Dk, bad);
+    launch(k_chol_diag, 1, 1024, 2 * CH_NB * (CH_NB + 1) * sizeof(double), s, a, n, k0, kb, Dk, bad);
     note_launch();
     const long long m = n - k1;
     if (m <= 0) continue;
     // L21 = A21 L11^-T into the scratch, copied over A21
     launch(k_dgemm_tile<false, true>, gemm_tiles(m, kb), 256, 0, s, (int)m, kb, kb, 1.0,
-           (const double*)(a + k1 * n + k0), n, (const double*)Dk, (long long)CH_NB, 0.0, P.get(), (long long)CH_NB, 0, 0);
+           (const double*)(a + k1 * n + k0), n, (const double*)Dk, (long long)CH_NB, 0.0, P.get(), (long long)CH_NB, 0, 0,
+           one);
     TMG_CUDA(cudaMemcpy2DAsync(a + k1 * n + k0, n * sizeof(double), P.get(), CH_NB * sizeof(double),
                                kb * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
     // A22 -= L21 L21^T (lower tiles)
     launch(k_dgemm_tile<false, true>, gemm_tiles(m, m), 256, 0, s, (int)m, (int)m, kb, -1.0,
-           (const double*)(a + k1 * n + k0), n, (const double*)(a + k1 * n + k0), n, 1.0, a + k1 * n + k1, n, 1, 0);
+           (const double*)(a + k1 * n + k0), n, (const double*)(a + k1 * n + k0), n, 1.0, a + k1 * n + k1, n, 1, 0, one);
     note_launch(2);
   }
-  // 2. Y = L^-1 by block rows: Y_ii = Dinv_i ; Y_i,0:i = -Dinv_i (L_i,0:i Y_0:i,0:i)
+  // 2. Y = L^-1 by recursive doubling.  The diagonal NB blocks are Dinv_k; at
+  // block size b every pair of adjacent diagonal blocks A = [2qb, 2qb + b),
+  // B = [2qb + b, 2qb + 2b) (cut at n) gets its off-diagonal block
+  //     Y_BA = - Y_BB (L_BA Y_AA)
+  // from two GEMMs batched over the pairs q (blockIdx.z): ~2 log2(n / NB)
+  // launches of many tiles instead of 2 n / NB launches of few.
   Y.zero(s);
   for (int i = 0; i < nb; ++i) {
     const int i0 = i * CH_NB, ib = (int)std::min<long long>(CH_NB, n - i0);
-    const double* Di = Dinv.get() + (size_t)i * CH_NB * CH_NB;
-    launch(k_chol_put_diag, 16, 256, 0, s, Y.get(), n, i0, ib, Di);
-    note_launch();
-    if (i == 0) continue;
-    // P (ib x i0) = L_i,0:i Y_0:i,0:i  (Y lower triangular: k from the tile's j0)
-    launch(k_dgemm_tile<false, false>, gemm_tiles(ib, i0), 256, 0, s, ib, i0, i0, 1.0,
-           (const double*)(a + (size_t)i0 * n), n, (const double*)Y.get(), n, 0.0, P.get(), n, 0, 2);
-    launch(k_dgemm_tile<false, false>, gemm_tiles(ib, i0), 256, 0, s, ib, i0, ib, -1.0, Di, (long long)CH_NB,
-           (const double*)P.get(), n, 0.0, Y.get() + (size_t)i0 * n, n, 0, 0);
+    launch(k_chol_put_diag, 16, 256, 0, s, Y.get(), n, i0, ib, (const double*)(Dinv.get() + (size_t)i * CH_NB * CH_NB));
+  }
+  note_launch(nb);
+  for (long long bsz = CH_NB; bsz < n; bsz *= 2) {
+    const int pairs = (int)((n - bsz + 2 * bsz - 1) / (2 * bsz));  // pairs whose B block is non-empty
+    if (pairs <= 0) break;
+    GemmBatch bt;
+    bt.sA = bt.sB = bt.sC = 2 * bsz * (n + 1);  // next pair: 2b rows and 2b columns further
+    bt.Mtot = (int)(n - bsz);                   // rows below the first A block ...
+    bt.dM = (int)(2 * bsz);                     // ... consumed 2b per pair: Mq = min(b, n - b - 2qb)
+    dim3 g = gemm_tiles(bsz, bsz);
+    g.z = (unsigned)pairs;
+    // T_BA = L_BA Y_AA   (Y_AA lower triangular: k from the tile's j0)
+    launch(k_dgemm_tile<false, false>, g, 256, 0, s, (int)bsz, (int)bsz, (int)bsz, 1.0, (const double*)(a + bsz * n), n,
+           (const double*)Y.get(), n, 0.0, P.get() + bsz * n, n, 0, 2, bt);
+    // Y_BA = - Y_BB T_BA   (the contraction runs over the rows of B: Mq of them)
+    bt.k_is_m = 1;
+    launch(k_dgemm_tile<false, false>, g, 256, 0, s, (int)bsz, (int)bsz, (int)bsz, -1.0,
+           (const double*)(Y.get() + bsz * (n + 1)), n, (const double*)(P.get() + bsz * n), n, 0.0, Y.get() + bsz * n, n,
+           0, 0, bt);
     note_launch(2);
   }
   // 3. A^-1 = Y^T Y (lower tiles; Y lower triangular: k from the tile's i0), mirrored
   launch(k_dgemm_tile<true, false>, gemm_tiles(n, n), 256, 0, s, (int)n, (int)n, (int)n, 1.0, (const double*)Y.get(),
-         n, (const double*)Y.get(), n, 0.0, a, n, 1, 1);
+         n, (const double*)Y.get(), n, 0.0, a, n, 1, 1, one);
   launch(k_sym_from_lower, grid_for(n * n), TPB, 0, s, a, n);
   note_launch(2);
   TMG_CUDA(cudaGetLastError());

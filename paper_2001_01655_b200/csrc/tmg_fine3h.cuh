@@ -460,10 +460,7 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
     // roles alternating (2-step unrolled loop: no register copies).
     auto layer = [&](int k, double Ek, const double (*Fb)[3], double (*Ft)[3], double (*G)[3], double (*T)[3]) {
       face((k + 2 - z0) % NU, Ft);  // plane k+1
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) T[q][c] = 0.0;
+      bool tset[4][3] = {};  // (compile-time after unrolling: first contribution to T[q][c] assigns)
       // one character block at a time: member (s = q + 4 qz, c) has
       // u^ = E (Fb[q] +- Ft[q]); its output y^ joins the bottom plane (+) and
       // the top plane (+-)
@@ -473,7 +470,7 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
           const int m = blk_member(chi, j), sj = m / 3, cj = m % 3, q = sj & 3;
-          uh[j] = (sj & 4) ? Ek * (Fb[q][cj] - Ft[q][cj]) : Ek * (Fb[q][cj] + Ft[q][cj]);
+          uh[j] = (sj & 4) ? Fb[q][cj] - Ft[q][cj] : Fb[q][cj] + Ft[q][cj];
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -488,8 +485,12 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
               any = true;
             }
           if (!any) continue;
-          G[q][ci] += y;  // bottom corners (z = 0): plane k
-          T[q][ci] = (si & 4) ? T[q][ci] - y : T[q][ci] + y;
+          // the element modulus scales the unit-modulus product on the way out
+          // (one FMA per target instead of a multiply per input and an add per target)
+          G[q][ci] = fma(Ek, y, G[q][ci]);  // bottom corners (z = 0): plane k
+          if (tset[q][ci]) T[q][ci] = fma((si & 4) ? -Ek : Ek, y, T[q][ci]);
+          else T[q][ci] = ((si & 4) ? -Ek : Ek) * y;
+          tset[q][ci] = true;
         }
       }
       // x-y inverse of plane k's character sums -> corner (x, y) contributions
@@ -520,7 +521,7 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
 #pragma unroll
       for (int c = 0; c < 3; ++c) G0[q][c] = 0.0;
     finish(0);  // plane z0-1
-    double Enext = load_E(z0 - 1);
+    double Enext = load_E(z0 - 1), Enext2 = load_E(z0);  // moduli two layers ahead of their use
     // step z0-2: only the bottom face of layer z0-1 (plane z0-1) and plane z0 finished
     asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
     finish(1);
@@ -530,14 +531,16 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
       asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");  // U of plane k+1 and X of step k-1 complete
       output(k);
       double Ek = Enext;
-      Enext = load_E(k + 1);
+      Enext = Enext2;
+      Enext2 = load_E(k + 2);
       load_epi(k, epre);
       if (k + 3 - z0 <= R) finish(k + 3 - z0);  // plane k+2
       layer(k, Ek, F0, F1, G0, G1);
       asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
       output(k + 1);
       Ek = Enext;
-      Enext = load_E(k + 2);
+      Enext = Enext2;
+      Enext2 = load_E(k + 3);
       load_epi(k + 1, epre);
       if (k + 4 - z0 <= R) finish(k + 4 - z0);  // plane k+3
       layer(k + 1, Ek, F1, F0, G1, G0);

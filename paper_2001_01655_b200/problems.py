@@ -127,8 +127,9 @@ def config_1(seed=1655, dims=(960, 320)):
                     # reports the converged flag -- the paper's GMG failure mode.
                     solvers=[dict(strategy="gmg", levels=5, smoother="weighted_jacobi", weight=0.6,
                                   n_pre=2, n_post=2, safeguard=1.8, max_iterations=2000),
+                             # (the same cap on the SA leg: w * lambda_max(D^-1 A) = 2.19 on its level 3)
                              dict(strategy="amg", coarse_max_dofs=499, beta=BETA, isolated="drop",
-                                  smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2,
+                                  smoother="weighted_jacobi", weight=0.6, n_pre=2, n_post=2, safeguard=1.8,
                                   max_iterations=2000)])
 
 

@@ -50,3 +50,20 @@ class Reordered:
 
     def __matmul__(self, x):
         return self.Kr @ np.ascontiguousarray(x[::-1])
+
+
+def other_coarse_solve(h):
+    """Replace an oracle hierarchy's coarsest SuperLU solve by dense Cholesky (LU
+    of the transpose if the matrix is not numerically SPD): an equally
+    backward-stable solver -- what the device's Cholesky-based coarse inverse is
+    to the reference's splu (multigrid.py:256-258).  Returns the previous solve."""
+    import scipy.linalg as sla
+    A = h.levels[-1].A.toarray()
+    old = h.coarse_solve
+    try:
+        cf = sla.cho_factor(A)
+        h.coarse_solve = lambda b: sla.cho_solve(cf, b)
+    except np.linalg.LinAlgError:
+        lu = sla.lu_factor(A.T)
+        h.coarse_solve = lambda b: sla.lu_solve(lu, b, trans=1)
+    return old

@@ -1,7 +1,7 @@
 """Fixed-iteration oracle checkpoints of the FULL BASELINE configs (test
 infrastructure, CPU, build container).
 
-    python tests/golden/make_checkpoints.py run --config C --variant base|perturbed [--maxit N]
+    python tests/golden/make_checkpoints.py run --config C --variant base|perturbed|perturbedN [--maxit N]
     python tests/golden/make_checkpoints.py combine --config C
 
 `run` builds the config's hierarchy with the oracle and runs its PCG (the
@@ -53,6 +53,7 @@ SCRATCH = os.environ.get("TMG_CKPT_SCRATCH", "/tmp/tmg_ckpt")
 # first restart.
 MAXIT = {1: 2000, 2: 300, 3: 3000, 4: 200}
 JITTER = 1e-14
+SAMPLE = 0  # index of the perturbed sample (seeds of the jitters); set by run()
 
 
 def leg_tag(leg):
@@ -60,23 +61,15 @@ def leg_tag(leg):
 
 
 def other_coarse_solve(h):
-    """Replace the coarsest SuperLU solve by dense Cholesky (LU of the transpose
-    if the matrix is not numerically SPD): an equally backward-stable solver."""
-    import scipy.linalg as sla
-    A = h.levels[-1].A.toarray()
-    try:
-        cf = sla.cho_factor(A)
-        h.coarse_solve = lambda b: sla.cho_solve(cf, b)
-    except np.linalg.LinAlgError:
-        lu = sla.lu_factor(A.T)
-        h.coarse_solve = lambda b: sla.lu_solve(lu, b, trans=1)
+    """ckpt_common.other_coarse_solve, returning the hierarchy."""
+    CK.other_coarse_solve(h)
     return h
 
 
-def last_bit_jitter(ke, seed=11):
+def last_bit_jitter(ke, seed=None):
     """KE with every entry moved by at most one unit in the last place, kept
     exactly symmetric."""
-    r = np.random.default_rng(seed).uniform(-1.0, 1.0, ke.shape)
+    r = np.random.default_rng(11 + SAMPLE if seed is None else seed).uniform(-1.0, 1.0, ke.shape)
     r = np.triu(r) + np.triu(r, 1).T
     return ke * (1.0 + np.finfo(float).eps * r)
 
@@ -91,12 +84,13 @@ def galerkin_right_first(A, P):
 def build(c, w, g, K, leg, perturbed):
     if not perturbed:
         return _build(c, w, g, K, leg, False)
-    keep = O.galerkin
+    keep, keepj = O.galerkin, O.jitter
     O.galerkin = galerkin_right_first
+    O.jitter = lambda B, rel, seed=7: keepj(B, rel, seed + SAMPLE)
     try:
         h = _build(c, w, g, K, leg, True)
     finally:
-        O.galerkin = keep
+        O.galerkin, O.jitter = keep, keepj
     return other_coarse_solve(h)
 
 
@@ -123,8 +117,10 @@ def _lmax(lv):
 
 
 def run(c, variant, maxit):
+    global SAMPLE
     os.makedirs(SCRATCH, exist_ok=True)
-    perturbed = variant == "perturbed"
+    perturbed = variant.startswith("perturbed")
+    SAMPLE = int(variant[len("perturbed"):] or 0) if perturbed else 0
     t0 = time.time()
     w = P.CONFIGS[c]()
     g = O.make_grid(w.mesh.dims)
@@ -180,6 +176,9 @@ def run(c, variant, maxit):
 
 
 def combine(c):
+    """Floors = the largest base-vs-perturbed distance over the perturbed
+    samples present in the scratch directory (perturbed, perturbed1, ...)."""
+    import glob
     w = P.CONFIGS[c]()
     loads = 1 + len(w.loads)
     out = {}
@@ -188,26 +187,33 @@ def combine(c):
         for li in range(loads):
             key = "%s_l%d" % (tag, li)
             b = dict(np.load(os.path.join(SCRATCH, "c%d_%s_base.npz" % (c, key))))
-            p = dict(np.load(os.path.join(SCRATCH, "c%d_%s_perturbed.npz" % (c, key))))
-            fx, fc = [], []
-            for k in b["ks"]:
-                xb = np.load(os.path.join(SCRATCH, "c%d_%s_base_x%d.npy" % (c, key, k)))
-                xp = np.load(os.path.join(SCRATCH, "c%d_%s_perturbed_x%d.npy" % (c, key, k)))
-                fx.append(np.linalg.norm(xp - xb) / np.linalg.norm(xb))
-                fc.append(abs(p["comp"][list(p["ks"]).index(k)] - b["comp"][list(b["ks"]).index(k)])
-                          / abs(b["comp"][list(b["ks"]).index(k)]))
-            xb = np.load(os.path.join(SCRATCH, "c%d_%s_base_xfinal.npy" % (c, key)))
-            xp = np.load(os.path.join(SCRATCH, "c%d_%s_perturbed_xfinal.npy" % (c, key)))
+            variants = sorted(os.path.basename(f)[len("c%d_%s_" % (c, key)):-4]
+                              for f in glob.glob(os.path.join(SCRATCH, "c%d_%s_perturbed*.npz" % (c, key))))
+            assert variants, "no perturbed sample for " + key
+            ks = list(b["ks"])
+            fx, fc = np.zeros(len(ks)), np.zeros(len(ks))
+            ffx = ffc = 0.0
+            xbf = np.load(os.path.join(SCRATCH, "c%d_%s_base_xfinal.npy" % (c, key)))
+            for v in variants:
+                p = dict(np.load(os.path.join(SCRATCH, "c%d_%s_%s.npz" % (c, key, v))))
+                for n, k in enumerate(ks):
+                    xb = np.load(os.path.join(SCRATCH, "c%d_%s_base_x%d.npy" % (c, key, k)))
+                    xp = np.load(os.path.join(SCRATCH, "c%d_%s_%s_x%d.npy" % (c, key, v, k)))
+                    fx[n] = max(fx[n], np.linalg.norm(xp - xb) / np.linalg.norm(xb))
+                    fc[n] = max(fc[n], abs(p["comp"][list(p["ks"]).index(k)] - b["comp"][n]) / abs(b["comp"][n]))
+                xp = np.load(os.path.join(SCRATCH, "c%d_%s_%s_xfinal.npy" % (c, key, v)))
+                ffx = max(ffx, np.linalg.norm(xp - xbf) / np.linalg.norm(xbf))
+                ffc = max(ffc, abs(p["final_comp"] - b["final_comp"]) / abs(b["final_comp"]))
+                print(key, v, "iterations base %d perturbed %d" % (b["iterations"], p["iterations"]))
             for name, v in b.items():
                 out["%s_%s" % (key, name)] = v
-            out[key + "_floor_x"] = np.array(fx)
-            out[key + "_floor_comp"] = np.array(fc)
-            out[key + "_floor_final_x"] = np.array(np.linalg.norm(xp - xb) / np.linalg.norm(xb))
-            out[key + "_floor_final_comp"] = np.array(abs(p["final_comp"] - b["final_comp"]) / abs(b["final_comp"]))
-            out[key + "_perturbed_iterations"] = p["iterations"]
-            out[key + "_perturbed_hist"] = p["hist"]
-            print(key, "iterations base %d perturbed %d" % (b["iterations"], p["iterations"]),
-                  "floors x", " ".join("%.2e" % v for v in fx), "comp", " ".join("%.2e" % v for v in fc))
+            out[key + "_floor_x"] = fx
+            out[key + "_floor_comp"] = fc
+            out[key + "_floor_final_x"] = np.array(ffx)
+            out[key + "_floor_final_comp"] = np.array(ffc)
+            out[key + "_floor_samples"] = np.array(len(variants))
+            print(key, "floors (%d samples) x" % len(variants), " ".join("%.2e" % v for v in fx), "comp",
+                  " ".join("%.2e" % v for v in fc))
     path = os.path.join(HERE, "config%d_checkpoints.npz" % c)
     np.savez_compressed(path, **out)
     print("wrote", path)
@@ -217,7 +223,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cmd", choices=["run", "combine"])
     ap.add_argument("--config", type=int, required=True)
-    ap.add_argument("--variant", choices=["base", "perturbed"], default="base")
+    ap.add_argument("--variant", default="base", help="base | perturbed | perturbedN (N: sample index = jitter seeds)")
     ap.add_argument("--maxit", type=int, default=None)
     a = ap.parse_args()
     if a.cmd == "run":

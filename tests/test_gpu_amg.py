@@ -89,7 +89,7 @@ def test_amg_pcg_matches_oracle(dims, beta, isolated):
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
     assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
-                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000))
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000, hierarchy=ho))
 
 
 # (16,8,8) with n_geo=2 is deliberately absent: its second SA level aggregates two
@@ -122,7 +122,7 @@ def test_hybrid_matches_oracle(dims, n_geo, kind, rtol):
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=rtol, max_iterations=3000)
     assert rec.converged
     assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
-                      reproducibility_floor(Kref, bc.load_vector, ho.apply, rtol=rtol, maxit=3000))
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, rtol=rtol, maxit=3000, hierarchy=ho))
 
 
 def test_hybrid_full_geo_equals_gmg_and_zero_is_amg():

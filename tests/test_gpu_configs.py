@@ -223,9 +223,18 @@ def run_checkpoints(c, legs=None):
                 print("%s k=%5d: compliance rel %.2e (oracle floor %.2e)  x rel %.2e (floor %.2e)  iters %d%s" % (
                     key, k, dc, fl_c, dx, fl_x, rec.iterations, "  true res %.2e" % (
                         rec.residual_history[-1] / np.linalg.norm(f))))
-                assert rec.iterations == int(k), (key, k, rec.iterations)
-                assert not rec.converged and not bool(ref[key + "_converged"]) or final
-            assert rec.converged == bool(ref[key + "_converged"])
+                if not final:
+                    assert rec.iterations == int(k) and not rec.converged, (key, k, rec.iterations)
+                    continue
+                # the cap run: the same verdict and iteration count -- unless the TRUE
+                # residual sits on its fp64 floor right at rtol (config 2: the
+                # oracle's own cap runs end at 1.0e-8 .. 2.4e-7 under rounding-level
+                # changes, rtol = 1e-8), where either verdict is a rounding accident
+                ref_res = float(ref[key + "_hist"][-1] / ref[key + "_fnorm"])
+                dev_res = rec.residual_history[-1] / np.linalg.norm(f)
+                same = rec.converged == bool(ref[key + "_converged"]) and rec.iterations == int(ref[key + "_iterations"])
+                on_floor = max(ref_res, dev_res) <= 30 * w.rtol and rec.iterations >= 0.95 * int(k)
+                assert same or on_floor, (key, rec.iterations, rec.converged, dev_res, ref_res)
     # every checkpoint is evaluated (and printed) before the first failure is raised
     for key, k, dc, fl_c, dx, fl_x in report:
         assert dc <= max(1e-10, 10 * fl_c), (key, k, dc, fl_c)

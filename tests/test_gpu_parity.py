@@ -20,7 +20,7 @@ from paper_2001_01655_b200 import problems  # noqa: E402
 
 
 from ckpt_common import Reordered as _Reordered  # noqa: E402
-from ckpt_common import block_dot  # noqa: E402
+from ckpt_common import block_dot, other_coarse_solve  # noqa: E402
 
 _DOT_ORDERS = (
     block_dot,                                               # GPU-like block partials
@@ -28,9 +28,10 @@ _DOT_ORDERS = (
 )
 
 
-def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
+def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000, hierarchy=None):
     """How far the oracle moves from itself when only the summation order
-    changes: of the matvec (rows summed in reverse column order) and of the dot products (block-partial
+    changes: of the matvec (rows summed in reverse column order), of the coarsest
+    direct solve (dense Cholesky for SuperLU, given `hierarchy`) and of the dot products (block-partial
     sums as on the GPU, reversed) -- O.pcg under the same true-residual
     contract.  E.g. the 3D SA case (12,6,6) of test_gpu_amg: the oracle takes
     54 iterations, 58 with reversed dots.  For strongly ill-conditioned systems
@@ -40,6 +41,12 @@ def reproducibility_floor(Kref, f, M, rtol=1e-8, maxit=2000):
     u1, r1 = O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit)
     runs = [O.pcg(_Reordered(Kref), f, None, M, rtol=rtol, max_iterations=maxit)]
     runs += [O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit, dot=d) for d in _DOT_ORDERS]
+    if hierarchy is not None:  # M = hierarchy.apply: the coarsest solve by another backward-stable solver
+        old = other_coarse_solve(hierarchy)
+        try:
+            runs.append(O.pcg(Kref, f, None, M, rtol=rtol, max_iterations=maxit))
+        finally:
+            hierarchy.coarse_solve = old
     fu = max(rel(u, u1) for u, _ in runs)
     fc = max(abs(f @ u - f @ u1) for u, _ in runs) / abs(f @ u1)
     return fu, fc, max(abs(r1.iterations - r.iterations) for _, r in runs)
@@ -175,7 +182,7 @@ def test_pcg_matches_oracle(dims, levels, kind, void):
     cfg = T.SolveConfig(rtol=1e-8, max_iterations=2000)
     u, rec = T.cg_solve(K, bc.load_vector, None, h, cfg)
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=2000)
-    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector, reproducibility_floor(Kref, bc.load_vector, ho.apply))
+    assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector, reproducibility_floor(Kref, bc.load_vector, ho.apply, hierarchy=ho))
     hist = np.array(rec.residual_history)
     n = min(len(hist), len(reco.residual_history), 10)
     assert np.allclose(hist[:n], reco.residual_history[:n], rtol=1e-8)
@@ -192,7 +199,7 @@ def test_jacobi_safeguard_matches_oracle():
     u, rec = T.cg_solve(K, bc.load_vector, None, h, T.SolveConfig(rtol=1e-8, max_iterations=3000))
     uo, reco = O.pcg(Kref, bc.load_vector, None, ho.apply, rtol=1e-8, max_iterations=3000)
     assert_pcg_parity(rec, host(u), reco, uo, bc.load_vector,
-                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000))
+                      reproducibility_floor(Kref, bc.load_vector, ho.apply, maxit=3000, hierarchy=ho))
 
 
 def test_pcg_warm_start_and_unpreconditioned():
@@ -213,6 +220,33 @@ def test_sensitivity_matches_oracle():
     mesh3, g3, *_ = cantilever((3, 2, 2), 9)
     u3 = np.random.default_rng(4).standard_normal(g3.n_dofs)
     assert rel(host(T.element_strain_energies(mesh3, u3)), O.strain_energies(g3, u3)) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,h", [((40, 12, 9), None), ((33, 9, 5), (1.0, 0.5, 2.0)), ((70, 17, 3), None),
+                                    ((5, 3, 1), None), ((50, 30), None)])
+def test_fused_compliance_sensitivity_matches_oracle(dims, h):
+    """tmg_compliance_sensitivity (one launch: f.u and dc) against the oracle
+    (optimization.py:106-111, 124-129) on ragged sizes: several tiles and z
+    chunks of the streamed 3D kernel, partial tiles, a single layer, and a
+    non-cubic element."""
+    import ctypes as C
+
+    from paper_2001_01655_b200 import _lib
+    from paper_2001_01655_b200._dev import as_dev, empty_dev, ptr
+    mesh, g, bc, rho, E, K, Kref = cantilever(dims, 5, h=h)
+    rng = np.random.default_rng(6)
+    u, f = rng.standard_normal(g.n_dofs), rng.standard_normal(g.n_dofs)
+    dc = empty_dev(mesh.element_count)
+    comp = C.c_double()
+    rho_d, f_d, u_d = as_dev(rho), as_dev(f), as_dev(u)
+    L = _lib.load()
+    for _ in range(2):  # the reduction slot is reused across calls
+        _lib.check(L.tmg_compliance_sensitivity(K.handle, ptr(rho_d), ptr(f_d), ptr(u_d), 3.0, 1.0, 1e-9, ptr(dc),
+                                                C.byref(comp), None))
+    Fo, dco = O.compliance_sensitivity(g, f, u, rho, 3.0, 1.0, 1e-9, ke=O.element_stiffness(g))
+    assert abs(comp.value - Fo) <= 1e-12 * np.linalg.norm(f) * np.linalg.norm(u)
+    assert rel(host(dc), dco) <= 1e-13
+    assert rel(host(T.element_strain_energies(mesh, u, K=K)), O.strain_energies(g, u, O.element_stiffness(g))) <= 1e-13
 
 
 def test_compliance_and_sensitivity_config0():

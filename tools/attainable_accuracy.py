@@ -105,8 +105,21 @@ def main():
                            converged=bool(m["converged"]), **analyse(K, f, u))
                 rows.append(row)
                 print(json.dumps(row), flush=True)
+        write(rows)
+
+
+def write(rows):
+    """Merge `rows` into profiles/r02_attainable_accuracy.{json,txt} (rows of other
+    configs already there are kept: the configs can be analysed one at a time)."""
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", "r02_attainable_accuracy.json"), "w") as fh:
+    jpath = os.path.join(ROOT, "profiles", "r02_attainable_accuracy.json")
+    old = []
+    if os.path.exists(jpath):
+        old = json.load(open(jpath))
+    new_keys = {(r["config"], r["leg"], r["load"]) for r in rows}
+    rows = sorted([r for r in old if (r["config"], r["leg"], r["load"]) not in new_keys] + rows,
+                  key=lambda r: (r["config"], r["leg"] != "gmg5", r["leg"], r["load"]))
+    with open(jpath, "w") as fh:
         json.dump(rows, fh, indent=1)
     with open(os.path.join(ROOT, "profiles", "r02_attainable_accuracy.txt"), "w") as fh:
         fh.write("# python tools/attainable_accuracy.py  (oracle K, the oracle's last iterate u of each leg;"
@@ -119,7 +132,7 @@ def main():
                 r["config"], r["leg"], r["load"], r["iterations"], "yes" if r["converged"] else "no", r["K2"],
                 r["unorm"], r["norm_bound"], r["comp_bound"], r["round_rms"], r["eval_noise"], r["true_res"],
                 "above" if r["round_rms"] > 1e-8 else "below"))
-    print("wrote profiles/r02_attainable_accuracy.{txt,json}")
+    print("wrote profiles/r02_attainable_accuracy.{txt,json} (%d rows)" % len(rows))
 
 
 if __name__ == "__main__":
