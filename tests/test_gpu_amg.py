@@ -96,10 +96,10 @@ def test_amg_pcg_matches_oracle(dims, beta, isolated):
 # 6-dof nodes whose candidate block [R_a; R_b] is rank deficient (exact zeros on
 # R's diagonal from the 2-node aggregates above), so the trailing Householder
 # columns of T are rounding noise in ANY implementation -- the reference is not
-# reproducible there either (tests/diagnostics/debug_hybrid.py shows the level-by-level split).
+# reproducible there either (diagnostics/debug_hybrid.py shows the level-by-level split).
 # (32,16): |u| = 3.6e8 with |f| = 1, so the fp64 floor of the TRUE residual,
 # ~eps |K| |u| = 8e-8, sits above rtol 1e-8 (device and oracle both stagnate at
-# 3e-8..1e-5 while restarting, tests/diagnostics/true_residual_gap.py): the case
+# 3e-8..1e-5 while restarting, diagnostics/true_residual_gap.py): the case
 # runs at rtol 1e-6, where both meet the reference's true-residual contract.
 @pytest.mark.parametrize("dims,n_geo,kind,rtol", [((16, 8, 8), 1, "weighted_jacobi", 1e-8),
                                                   ((16, 8, 8), 1, "chebyshev", 1e-8),

@@ -1,9 +1,10 @@
 #!/bin/bash
-# One GPU round trip: parity suite, per-leg timings of a config, short bench.
+# One GPU round trip (gpurun -- 'bash tools/gpu_round.sh'): parity suite with the
+# checkpoint table, smoke, default bench, per-level breakdown of configs 3 and 4.
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-for c in ${CONFIGS:-1}; do
-  TMG_VERBOSE=1 timeout 600 python tools/profile_case.py --config $c --iters ${ITERS:-3000} > gpurun_out/profile_c$c.log 2>&1
-done
-timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.log
+( time timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -s ) 2>&1 | grep -E "k=|passed|failed|Error|real" > gpurun_out/pytest_gpu_all.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+( time timeout 900 python bench.py ) > gpurun_out/bench.log 2>&1
+for c in ${CONFIGS:-4 3}; do timeout 600 python tools/iter_breakdown.py --config $c > gpurun_out/iter_breakdown_c$c.txt 2>&1; done
 echo done

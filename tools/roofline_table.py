@@ -20,7 +20,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 F8 = 8
-FP64_PEAK_TF = 37.0  # B200 dense FP64 (vector) peak, NVIDIA datasheet figure (not measured here)
+def _fp64_peak():
+    """Measured DFMA peak of the pool's B200 (tools/fp64_peak.cu -> profiles/r02_fp64_peak.json)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")))["fp64_dfma_tflops"])
+    except Exception:  # noqa: BLE001
+        return 34.2
+
+
+FP64_PEAK_TF = _fp64_peak()
+# FP64 pipe instructions per element of the character-basis Hex8 operator
+# (tmg_fine3h.cuh): 24 face-transform adds, 24 z-combinations, 45 KE^ terms, 42
+# accumulations, 24 inverse-transform adds, 6 neighbour adds (+ ~10 epilogue);
+# each occupies one issue slot of the FP64 pipe whether it is an add or an FMA,
+# so the pipe fraction is instructions / (peak FMA rate)
+F3H_DP_PER_ELEMENT = 175.0
 
 
 def level_bytes(h, k, ndim, mesh, n_levels):
@@ -103,10 +117,12 @@ def main():
                            us=t * 1e3, gbs=gbs, frac=gbs / peak)
                 extra = ""
                 if lv.storage == "matrix_free" and w.mesh.ndim == 3 and nm in ("sweep", "residual"):
-                    # the Hex8 operator is FP64-bound: 576 FMA per node (24x24 KE per element)
-                    tf = 2.0 * 576 * w.mesh.node_count / (t * 1e-3) / 1e12
-                    row.update(fp64_tflops=tf, fp64_frac=tf / FP64_PEAK_TF)
-                    extra = "   FP64 %.1f TF/s = %.2f of %.0f" % (tf, tf / FP64_PEAK_TF, FP64_PEAK_TF)
+                    # FP64-pipe occupancy of the Hex8 operator: DP instructions per
+                    # second against the measured DFMA issue rate (peak TF/s / 2)
+                    gi = F3H_DP_PER_ELEMENT * w.mesh.element_count / (t * 1e-3) / 1e12
+                    row.update(fp64_tinstr=gi, fp64_frac=gi / (FP64_PEAK_TF / 2))
+                    extra = "   FP64 pipe %.2f T instr/s = %.2f of the measured %.1f (= %.1f TF/s / 2)" % (
+                        gi, gi / (FP64_PEAK_TF / 2), FP64_PEAK_TF / 2, FP64_PEAK_TF)
                 rows.append(row)
                 print("  %-6s %3d %-11s %9d  %-9s %10d %8.2f %9.0f %6.2f%s" % (lr.name, k, lv.storage, lv.size, nm, by,
                                                                              t * 1e3, gbs, gbs / peak, extra),
