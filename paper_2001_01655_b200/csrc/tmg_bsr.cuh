@@ -231,18 +231,24 @@ __global__ void k_bsr_cheb_p(const double* __restrict__ r, const double* __restr
 // The last step of a Chebyshev pass whose residual r' nobody reads: only
 // x += alpha p' with p' = D^-1 r + beta p remains -- a vector update, no
 // operator application (any level storage; same arithmetic as the full step).
+// bdot != nullptr: also reduce sum(x' . bdot) into red (the PCG r.z when this is
+// the last kernel of the level-0 V-cycle; grid <= the reduction's partial slots).
 __global__ void k_cheb_x_only(const double* __restrict__ r, const double* __restrict__ p,
                               const double* __restrict__ dinv, const double* __restrict__ coef, int step, int x_zero,
-                              double* __restrict__ x, long long n) {
+                              double* __restrict__ x, long long n, const double* __restrict__ bdot, Red red) {
   TMG_PDL_ENTRY;
   const double alpha = coef[2 * step], beta = step == 0 ? 0.0 : coef[2 * step + 1];
   const long long stride = (long long)gridDim.x * blockDim.x;
+  double v = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
     const double z = dinv ? dinv[i] * r[i] : r[i];
     const double pv = beta == 0.0 ? z : z + beta * p[i];
     const double x0 = x_zero ? 0.0 : x[i];
-    x[i] = x0 + alpha * pv;
+    const double xn = x0 + alpha * pv;
+    x[i] = xn;
+    if (bdot) v += xn * bdot[i];
   }
+  if (bdot) grid_reduce(v, red);
 }
 template <int R>
 __global__ void __launch_bounds__(TPB, TMG_BSR_MINB) k_bsr_cheb(BsrView<R, R> A, const double* __restrict__ r,

@@ -84,7 +84,10 @@ __host__ __device__ constexpr int blk_coef(int chi, int i, int j) {
 }
 constexpr int NC = NT;               // consumer threads (8 warps)
 constexpr int NTH = NT + 32;         // + the producer warp
-constexpr int NSR = 3;               // raw plane ring (TMA destination)
+#ifndef TMG_F3H_NSR
+#define TMG_F3H_NSR 3
+#endif
+constexpr int NSR = TMG_F3H_NSR;     // raw plane ring (TMA destination)
 constexpr int NU = 4;                // finished plane ring (written 2 steps ahead, read 2 steps behind)
 constexpr int NVS = 3, NVE = 2;      // max source / epilogue vectors
 constexpr int ROWD = 104;            // doubles per staged row buffer (33 nodes x 3 + alignment shift, 16-B multiple)
@@ -233,6 +236,91 @@ struct EpiIn {
   const double* v[NVE];  // epilogue input vectors (3 doubles per node); nullptr = not used
 };
 }  // namespace f3h
+template <int DIM>
+struct FineOp;
+namespace f3h {
+// The producer warp (32 lanes): streams the raw planes z0-1 .. z0-1+R of the
+// (TX+1) x (TY+1) node window into the NSR-deep ring with TMA bulk copies
+// (rows whose 16-B aligned window would leave the vector: plain loads).
+template <class Src>
+__device__ __forceinline__ void produce(const FineOp<3>& op, const Src& src, double* SR, unsigned char* MR,
+                                        unsigned long long* raw_full, unsigned long long* raw_free, int lane, int z0,
+                                        int R, int j0, int nlo, int ncnt) {
+  const int nn0 = op.L.nn[0], nn1 = op.L.nn[1], nn2 = op.L.nn[2];
+  const long long plane = (long long)nn0 * nn1;
+  const long long ndof = 3 * op.L.n;
+  constexpr int NTASK = NVS * SY + SY;  // source rows, mask rows
+  for (int r = 0; r <= R; ++r) {
+    const int p = z0 - 1 + r, s3 = r % NSR;
+    if (r >= NSR) {
+      if (lane == 0) mbar_wait(raw_free + s3, (unsigned)((r / NSR) - 1) & 1u);
+      __syncwarp();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const bool pin = p >= 0 && p < nn2;
+    Row rw[2];
+    void* dst[2];
+    const char* gend[2];
+    int isz[2];
+    unsigned tx = 0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int q = lane + 32 * u;
+      rw[u].bytes = 0;
+      rw[u].tma = false;
+      dst[u] = nullptr;
+      gend[u] = nullptr;
+      isz[u] = 8;
+      if (q >= NTASK || !pin) continue;
+      if (q < NVS * SY) {
+        const int v = q / SY, row = q % SY, gj = j0 + row;
+        const double* vp = v < Src::NV ? src.vec(v) : nullptr;
+        if (!vp || gj < 0 || gj >= nn1) continue;
+        rw[u] = row_window(vp + 3 * (p * plane + (long long)gj * nn0 + nlo), 3 * ncnt, 8, vp, vp + ndof);
+        dst[u] = SR + ((s3 * NVS + v) * SY + row) * ROWD;
+        gend[u] = (const char*)(vp + ndof);
+      } else {
+        const int row = q - NVS * SY, gj = j0 + row;
+        if (gj < 0 || gj >= nn1) continue;
+        rw[u] = row_window(op.mask + p * plane + (long long)gj * nn0 + nlo, ncnt, 1, op.mask, op.mask + op.L.n);
+        dst[u] = MR + (s3 * SY + row) * MROW;
+        gend[u] = (const char*)(op.mask + op.L.n);
+        isz[u] = 1;
+      }
+      if (rw[u].tma) tx += rw[u].bytes;
+    }
+    tx = __reduce_add_sync(0xffffffffu, tx);
+    if (lane == 0) mbar_expect_tx(raw_full + s3, tx);  // the arrival follows the plain-copy rows
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (rw[u].tma) bulk_g2s(dst[u], rw[u].a0, rw[u].bytes, raw_full + s3);
+    // rows whose aligned window would leave the vector (its first / last
+    // row): the warp copies the items with plain loads into the same layout,
+    // published by the warp's arrival below (release)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      unsigned need = __ballot_sync(0xffffffffu, rw[u].bytes > 0 && !rw[u].tma);
+      while (need) {
+        const int l = __ffs(need) - 1;
+        need &= need - 1;
+        const char* g = (const char*)__shfl_sync(0xffffffffu, (unsigned long long)rw[u].a0, l);
+        const int shift = __shfl_sync(0xffffffffu, rw[u].shift, l);
+        const unsigned bytes = __shfl_sync(0xffffffffu, rw[u].bytes, l);
+        const char* ge = (const char*)__shfl_sync(0xffffffffu, (unsigned long long)gend[u], l);
+        const int sz = __shfl_sync(0xffffffffu, isz[u], l);
+        unsigned char* d = (unsigned char*)__shfl_sync(0xffffffffu, (unsigned long long)dst[u], l);
+        for (int b = shift + lane * sz; b < (int)bytes && g + b < ge; b += 32 * sz) {
+          if (sz == 1) d[b] = *(const unsigned char*)(g + b);
+          else *reinterpret_cast<double*>(d + b) = *reinterpret_cast<const double*>(g + b);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(raw_full + s3);
+  }
+}
+}  // namespace f3h
 
 template <class Src, class Epi>
 __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src, const f3h::EpiIn& ein, Epi&& epi) {
@@ -268,78 +356,7 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
   const long long ndof = 3 * op.L.n;
 
   if (t >= NC) {
-    // ===================== producer warp: TMA of the raw planes =====================
-    const int lane = t - NC;
-    constexpr int NTASK = NVS * SY + SY;  // source rows, mask rows
-    for (int r = 0; r <= R; ++r) {
-      const int p = z0 - 1 + r, s3 = r % NSR;
-      if (r >= NSR) {
-        if (lane == 0) mbar_wait(raw_free + s3, (unsigned)((r / NSR) - 1) & 1u);
-        __syncwarp();
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const bool pin = p >= 0 && p < nn2;
-      Row rw[2];
-      void* dst[2];
-      const char* gend[2];
-      int isz[2];
-      unsigned tx = 0;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int q = lane + 32 * u;
-        rw[u].bytes = 0;
-        rw[u].tma = false;
-        dst[u] = nullptr;
-        gend[u] = nullptr;
-        isz[u] = 8;
-        if (q >= NTASK || !pin) continue;
-        if (q < NVS * SY) {
-          const int v = q / SY, row = q % SY, gj = j0 + row;
-          const double* vp = v < Src::NV ? src.vec(v) : nullptr;
-          if (!vp || gj < 0 || gj >= nn1) continue;
-          rw[u] = row_window(vp + 3 * (p * plane + (long long)gj * nn0 + nlo), 3 * ncnt, 8, vp, vp + ndof);
-          dst[u] = SR + ((s3 * NVS + v) * SY + row) * ROWD;
-          gend[u] = (const char*)(vp + ndof);
-        } else {
-          const int row = q - NVS * SY, gj = j0 + row;
-          if (gj < 0 || gj >= nn1) continue;
-          rw[u] = row_window(op.mask + p * plane + (long long)gj * nn0 + nlo, ncnt, 1, op.mask, op.mask + op.L.n);
-          dst[u] = MR + (s3 * SY + row) * MROW;
-          gend[u] = (const char*)(op.mask + op.L.n);
-          isz[u] = 1;
-        }
-        if (rw[u].tma) tx += rw[u].bytes;
-      }
-      tx = __reduce_add_sync(0xffffffffu, tx);
-      if (lane == 0) mbar_expect_tx(raw_full + s3, tx);  // the arrival follows the plain-copy rows
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (rw[u].tma) bulk_g2s(dst[u], rw[u].a0, rw[u].bytes, raw_full + s3);
-      // rows whose aligned window would leave the vector (its first / last
-      // row): the warp copies the items with plain loads into the same layout,
-      // published by the warp's arrival below (release)
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        unsigned need = __ballot_sync(0xffffffffu, rw[u].bytes > 0 && !rw[u].tma);
-        while (need) {
-          const int l = __ffs(need) - 1;
-          need &= need - 1;
-          const char* g = (const char*)__shfl_sync(0xffffffffu, (unsigned long long)rw[u].a0, l);
-          const int shift = __shfl_sync(0xffffffffu, rw[u].shift, l);
-          const unsigned bytes = __shfl_sync(0xffffffffu, rw[u].bytes, l);
-          const char* ge = (const char*)__shfl_sync(0xffffffffu, (unsigned long long)gend[u], l);
-          const int sz = __shfl_sync(0xffffffffu, isz[u], l);
-          unsigned char* d = (unsigned char*)__shfl_sync(0xffffffffu, (unsigned long long)dst[u], l);
-          for (int b = shift + lane * sz; b < (int)bytes && g + b < ge; b += 32 * sz) {
-            if (sz == 1) d[b] = *(const unsigned char*)(g + b);
-            else *reinterpret_cast<double*>(d + b) = *reinterpret_cast<const double*>(g + b);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(raw_full + s3);
-    }
+    produce<Src>(op, src, SR, MR, raw_full, raw_free, t - NC, z0, R, j0, nlo, ncnt);
   } else {
     // ===================== consumer warps =====================
     const int tx = t % TX, ty = t / TX;

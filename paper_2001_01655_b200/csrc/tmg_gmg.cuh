@@ -624,7 +624,7 @@ std::unique_ptr<Hierarchy> build_smoother(const Operator& K, const SmootherCfg& 
 // b - A x, multigrid.py:238-239; the two differ by fp64 rounding only).
 template <int DIM>
 const double* smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bool x_zero, int passes,
-                          cudaStream_t s, bool want_r = false) {
+                          cudaStream_t s, bool want_r = false, const Red* dot = nullptr, bool* dot_done = nullptr) {
   const double* rlast = nullptr;
   for (int p = 0; p < passes; ++p) {
     const double* rin;
@@ -659,9 +659,14 @@ const double* smooth_cheb(Hierarchy& H, Level& l, const double* b, double* x, bo
       }();
       if (last && !keep_r && x_only) {
         // neither p' nor r' of this step is read: x += alpha p' needs no operator application
-        launch(k_cheb_x_only, grid_for(l.ndof), TPB, 0, s, zs, pin, dv, (const double*)l.coef.get(), i,
-               (x_zero && i == 0) ? 1 : 0, x, l.ndof);
+        // (the very last kernel of a level-0 V-cycle inside PCG also reduces r.z = x'.b)
+        const bool with_dot = dot != nullptr && p + 1 == passes;
+        const Red nored{nullptr, nullptr, nullptr};
+        launch(k_cheb_x_only, with_dot ? std::min<unsigned>(grid_for(l.ndof), RED_BLOCKS * 4u) : grid_for(l.ndof), TPB, 0,
+               s, zs, pin, dv, (const double*)l.coef.get(), i, (x_zero && i == 0) ? 1 : 0, x, l.ndof,
+               with_dot ? b : (const double*)nullptr, with_dot ? *dot : nored);
         note_launch();
+        if (with_dot && dot_done) *dot_done = true;
       } else {
         lvl_cheb_step<DIM>(l, rin, zs, dv, pin, i, x_zero && i == 0, x, po, keep_r ? ro : nullptr, s, !last);
       }
@@ -719,9 +724,10 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
     return !(e && e[0] == '0');  // 0: recompute b - A x after pre-smoothing (the reference's order of work)
   }();
   const double* r_pre = nullptr;
-  auto smooth_poly = [&](double* x, bool x_zero, int passes, bool want_r) {
+  bool cheb_dot = false;
+  auto smooth_poly = [&](double* x, bool x_zero, int passes, bool want_r, const Red* d = nullptr) {
     if (H.sm.kind == SM_SOR_GMRES) smooth_sor_gmres<DIM>(H, l, b, x, x_zero, passes, s);
-    else r_pre = smooth_cheb<DIM>(H, l, b, x, x_zero, passes, s, want_r && reuse_r);
+    else r_pre = smooth_cheb<DIM>(H, l, b, x, x_zero, passes, s, want_r && reuse_r, d, &cheb_dot);
   };
   const int W = H.n_pre + H.n_post;
   auto buf = [&](int w) { return ((W - w) % 2 == 0) ? xout : l.xt.get(); };
@@ -766,7 +772,9 @@ bool vcycle(Hierarchy& H, int k, const double* b, double* xout, cudaStream_t s, 
                             (fuse_mode == 2 || (fuse_mode == 1 && l.opkind == OP_FINE));
   if (!fuse_prolong) xfer_prolong_add<DIM>(H, k, xcur, s);
   if (cheb) {
-    smooth_poly(xcur, false, H.n_post, false);
+    // (the dot is valid only if the smoothed vector IS the V-cycle's output buffer)
+    smooth_poly(xcur, false, H.n_post, false, (dot && xcur == xout && H.n_post > 0) ? dot : nullptr);
+    dot_done |= cheb_dot;
   } else {
     for (int p = 0; p < H.n_post; ++p) {
       double* dst = buf(++widx);

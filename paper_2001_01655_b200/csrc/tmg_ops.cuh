@@ -323,6 +323,9 @@ struct FineOp {
 #if defined(TMG_FINE3_TILE)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
   static constexpr int THREADS = TPB;
+#elif defined(TMG_F3P)
+  static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : 1;  // 3D: one CTA per SM (tmg_fine3p.cuh)
+  static constexpr int THREADS = DIM == 2 ? TPB : 64 * TMG_F3H_TY + 32;  // 3D: a warp pair per row + the TMA producer warp
 #elif !defined(TMG_F3S)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;  // 3D: one CTA per SM (tmg_fine3h.cuh)
   static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3H_TY + 32;  // 3D: consumer warps + the TMA producer warp
@@ -555,18 +558,25 @@ struct FineOp {
 }  // namespace tmg
 #include "tmg_fine3h.cuh"
 #include "tmg_fine3s.cuh"
+#include "tmg_fine3p.cuh"
 namespace tmg {
 // the streamed 3D row path (FineOp<3>::STREAM): character-basis elements, the
 // epilogue's input vectors staged by the producer warp (ein)
 template <class Src, class Epi>
 __device__ __forceinline__ void fine3_rows(const FineOp<3>& op, const Src& src, const f3h::EpiIn& ein, Epi&& epi) {
-#ifndef TMG_F3S
+#if defined(TMG_F3P)
+  fine3p_rows(op, src, ein, static_cast<Epi&&>(epi));
+#elif !defined(TMG_F3S)
   fine3h_rows(op, src, ein, static_cast<Epi&&>(epi));
 #else
   fine3s_rows(op, src, ein, static_cast<Epi&&>(epi));
 #endif
 }
-#ifndef TMG_F3S
+#if defined(TMG_F3P)
+inline dim3 fine3_grid(const Lat& L) { return f3h::grid(L); }
+constexpr int fine3_threads() { return f3p::NTHP; }
+constexpr size_t fine3_smem() { return f3p::SMEM_BYTES_P; }
+#elif !defined(TMG_F3S)
 inline dim3 fine3_grid(const Lat& L) { return f3h::grid(L); }
 constexpr int fine3_threads() { return f3h::NTH; }
 constexpr size_t fine3_smem() { return f3h::SMEM_BYTES; }
