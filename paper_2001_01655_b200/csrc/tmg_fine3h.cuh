@@ -83,7 +83,16 @@ __host__ __device__ constexpr int blk_coef(int chi, int i, int j) {
   return K[(chi * 3 + i) * 3 + j];
 }
 constexpr int NC = NT;               // consumer threads (8 warps)
-constexpr int NTH = NT + 32;         // + the producer warp
+#ifndef TMG_F3H_NSR
+#define TMG_F3H_NSR 3
+#endif
+#define TMG_F3H_NSR_MAXP TMG_F3H_NSR
+#ifndef TMG_F3H_NPROD
+#define TMG_F3H_NPROD 3  // producer warps (planes dealt round-robin; 3: config-4 PCG iteration -2.5 % vs 1)
+#endif
+constexpr int NPROD = TMG_F3H_NPROD;
+constexpr int NTH = NT + 32 * NPROD;  // + the producer warp(s)
+static_assert(NPROD >= 1 && NPROD <= TMG_F3H_NSR_MAXP, "at most one producer warp per ring slot");
 #ifndef TMG_F3H_NSR
 #define TMG_F3H_NSR 3
 #endif
@@ -201,6 +210,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+// (producer side: the slot frees up about once per layer -- back off between polls
+// instead of competing with the consumer warps for issue slots)
+__device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(200);
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -245,15 +270,15 @@ namespace f3h {
 template <class Src>
 __device__ __forceinline__ void produce(const FineOp<3>& op, const Src& src, double* SR, unsigned char* MR,
                                         unsigned long long* raw_full, unsigned long long* raw_free, int lane, int z0,
-                                        int R, int j0, int nlo, int ncnt) {
+                                        int R, int j0, int nlo, int ncnt, int r0 = 0, int rstep = 1) {
   const int nn0 = op.L.nn[0], nn1 = op.L.nn[1], nn2 = op.L.nn[2];
   const long long plane = (long long)nn0 * nn1;
   const long long ndof = 3 * op.L.n;
   constexpr int NTASK = NVS * SY + SY;  // source rows, mask rows
-  for (int r = 0; r <= R; ++r) {
+  for (int r = r0; r <= R; r += rstep) {
     const int p = z0 - 1 + r, s3 = r % NSR;
     if (r >= NSR) {
-      if (lane == 0) mbar_wait(raw_free + s3, (unsigned)((r / NSR) - 1) & 1u);
+      if (lane == 0) mbar_wait_backoff(raw_free + s3, (unsigned)((r / NSR) - 1) & 1u);
       __syncwarp();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -356,7 +381,7 @@ __device__ __forceinline__ void fine3h_rows(const FineOp<3>& op, const Src& src,
   const long long ndof = 3 * op.L.n;
 
   if (t >= NC) {
-    produce<Src>(op, src, SR, MR, raw_full, raw_free, t - NC, z0, R, j0, nlo, ncnt);
+    produce<Src>(op, src, SR, MR, raw_full, raw_free, (t - NC) & 31, z0, R, j0, nlo, ncnt, (t - NC) >> 5, NPROD);
   } else {
     // ===================== consumer warps =====================
     const int tx = t % TX, ty = t / TX;

@@ -22,7 +22,7 @@ namespace tmg {
 namespace f3p {
 using namespace f3h;
 constexpr int NCP = 2 * NT;          // consumer threads (16 warps)
-constexpr int NTHP = NCP + 32;       // + the producer warp
+constexpr int NTHP = NCP + 32 * NPROD;  // + the producer warps
 constexpr size_t OFF_Z = al128(f3h::SMEM_BYTES);                 // [2 (half)][6][NT] partial sums
 constexpr size_t SMEM_BYTES_P = OFF_Z + sizeof(double) * 2 * 6 * NT;
 static_assert(SMEM_BYTES_P <= 227 * 1024 - 2048, "f3p shared memory");
@@ -285,8 +285,8 @@ __device__ __forceinline__ void fine3p_rows(const FineOp<3>& op, const Src& src,
   }
   __syncthreads();
   if (t >= NCP) {
-    produce<Src>(op, src, reinterpret_cast<double*>(f3p_raw + OFF_SRAW), f3p_raw + OFF_MRAW, raw_full, raw_free, t - NCP,
-                 z0, R, j0, nlo, ncnt);
+    produce<Src>(op, src, reinterpret_cast<double*>(f3p_raw + OFF_SRAW), f3p_raw + OFF_MRAW, raw_full, raw_free,
+                 (t - NCP) & 31, z0, R, j0, nlo, ncnt, (t - NCP) >> 5, NPROD);
   } else {
     const int w = t >> 5, h = w & 1;                 // warp pair (row) w / 2, half h
     const int tb = (t & 31) + 32 * (w >> 1);         // tx + 32 ty

@@ -278,6 +278,10 @@ struct FineOp {
   // one-node halo: the source vector (unmasked), the free-dof masks and the
   // moduli of the (BX+1)(BY+1)(BZ+1) elements touching the tile.  Every value is
   // read from L2/HBM once per block instead of once per neighbouring thread.
+// 3D level-0 variant: the paired-warp stream (tmg_fine3p.cuh) unless another is asked for
+#if !defined(TMG_F3P) && !defined(TMG_F3H) && !defined(TMG_F3S) && !defined(TMG_FINE3_TILE)
+#define TMG_F3P 1
+#endif
 #ifndef TMG_F3_BX
 #define TMG_F3_BX 16
 #define TMG_F3_BY 4
@@ -324,11 +328,17 @@ struct FineOp {
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3_MINB;
   static constexpr int THREADS = TPB;
 #elif defined(TMG_F3P)
+#ifndef TMG_F3H_NPROD
+#define TMG_F3H_NPROD 3
+#endif
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : 1;  // 3D: one CTA per SM (tmg_fine3p.cuh)
-  static constexpr int THREADS = DIM == 2 ? TPB : 64 * TMG_F3H_TY + 32;  // 3D: a warp pair per row + the TMA producer warp
+  static constexpr int THREADS = DIM == 2 ? TPB : 64 * TMG_F3H_TY + 32 * TMG_F3H_NPROD;  // 3D: a warp pair per row + the TMA producer warps
 #elif !defined(TMG_F3S)
   static constexpr int MINB = DIM == 2 ? TMG_F2_MINB : TMG_F3H_MINB;  // 3D: one CTA per SM (tmg_fine3h.cuh)
-  static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3H_TY + 32;  // 3D: consumer warps + the TMA producer warp
+#ifndef TMG_F3H_NPROD
+#define TMG_F3H_NPROD 3
+#endif
+  static constexpr int THREADS = DIM == 2 ? TPB : 32 * TMG_F3H_TY + 32 * TMG_F3H_NPROD;  // 3D: consumer warps + the TMA producer warp(s)
 #else
 #ifndef TMG_F3S_TY
 #define TMG_F3S_TY 8

@@ -37,8 +37,9 @@ FP64_PEAK_TF = _fp64_peak()
 F3H_DP_PER_ELEMENT = 175.0
 
 
-def level_bytes(h, k, ndim, mesh, n_levels):
-    """(sweep, residual, restrict, prolong) algorithmic bytes of level k."""
+def level_bytes(h, k, ndim, mesh, n_levels, cheb=False):
+    """(sweep, residual, restrict, prolong) algorithmic bytes of level k.  cheb: the
+    timed sweep is one Chebyshev step (r, D^-1, p, x in; x, p', r' out)."""
     lv = h.levels[k]
     n = lv.size
     nxt = h.levels[k + 1].size if k + 1 < n_levels else 0
@@ -53,7 +54,7 @@ def level_bytes(h, k, ndim, mesh, n_levels):
         _lib.check(_lib.load().tmg_hierarchy_export(h.handle, k, 0, dims, None, None, None, None))
         nnzb = int(dims[2])
         op = lv.nonzeros * F8 + nnzb * 4 + (int(dims[0]) + 1) * 4
-    sweep = op + 4 * n * F8  # x, b, D^-1 in; x' out
+    sweep = op + (7 if cheb else 4) * n * F8  # Jacobi: x, b, D^-1 in; x' out.  Chebyshev step: 4 in, 3 out
     resid = op + 3 * n * F8  # x, b in; r out
     if lv.provenance == "geometric" or k + 1 >= n_levels:
         restrict = n * F8 + 3 * nxt * F8  # r in; b_c, x_c out, D_c^-1 in
@@ -104,7 +105,7 @@ def main():
                 _lib.check(L.tmg_hierarchy_time_phase(h.handle, k, 3, a.reps, C.byref(ms), None))
                 phases = [("coarse", lv.size * lv.size * F8 if k > 0 else 0, ms.value)]
             else:
-                b = level_bytes(h, k, w.mesh.ndim, w.mesh, nl)
+                b = level_bytes(h, k, w.mesh.ndim, w.mesh, nl, cheb=leg["smoother"] == "chebyshev")
                 phases = []
                 _lib.check(L.tmg_hierarchy_time_smoother(h.handle, k, a.reps, C.byref(ms), None))
                 phases.append(("sweep", b[0], ms.value))
