@@ -326,6 +326,95 @@ __global__ void __launch_bounds__(sens3::NT, 2) k_sens3(const __grid_constant__ 
   if (f) grid_reduce(dot, red);
 }
 
+// The 3D form of k_sens on bricks: a CTA owns 32 x 4 x 2 elements, one per
+// thread.  The brick's 33 x 5 x 3 nodes are staged ONCE in shared memory by
+// coalesced row loads (15 rows of 99 contiguous doubles), so an element costs
+// 24 conflict-free shared loads instead of 24 strided global ones and every load
+// of the CTA is in flight at once (no dependent steps: latency is hidden by the
+// ~7000 independent CTAs).  The compliance f.u is reduced from the staged values
+// (every node is owned by exactly one brick), so u is read from HBM once.
+namespace sensb {
+constexpr int BX = 32, BY = 4, BZ = 2, NT = BX * BY * BZ;
+constexpr int NRX = 3 * (BX + 1), NROW = (BY + 1) * (BZ + 1);  // doubles per staged row, rows per brick
+constexpr int PITCH = NRX + 1;                                 // (100 doubles: rows 8 banks apart)
+constexpr int NLD = (NRX * NROW + NT - 1) / NT;                // staged doubles per thread
+}  // namespace sensb
+__global__ void __launch_bounds__(sensb::NT, 3) k_sensb(const __grid_constant__ FineOp<3> op,
+                                                        const double* __restrict__ u, const double* __restrict__ f,
+                                                        double* __restrict__ ce, const double* __restrict__ rho,
+                                                        double p, double e0, double emin, double* __restrict__ dc,
+                                                        Red red) {
+  TMG_PDL_ENTRY;
+  using namespace sensb;
+  __shared__ double sm[NROW * PITCH];
+  const int t = threadIdx.x;
+  const int nn0 = op.L.nn[0], nn1 = op.L.nn[1], nn2 = op.L.nn[2];
+  const int ne0 = op.ne[0], ne1 = op.ne[1], ne2 = op.ne[2];
+  const int i0 = blockIdx.x * BX, j0 = blockIdx.y * BY, k0 = blockIdx.z * BZ;
+  double dot = 0.0;
+#pragma unroll
+  for (int l = 0; l < NLD; ++l) {
+    const int idx = t + l * NT;
+    if (idx >= NRX * NROW) break;
+    const int row = idx / NRX, q = idx - row * NRX;
+    const int ry = row % (BY + 1), rz = row / (BY + 1);
+    const int gi = i0 + q / 3, gj = j0 + ry, gk = k0 + rz;
+    double v = 0.0;
+    if (gi < nn0 && gj < nn1 && gk < nn2) {
+      const long long g = 3 * (((long long)gk * nn1 + gj) * nn0 + i0) + q;
+      v = __ldg(u + g);
+      const bool own = (q < 3 * BX || gi == nn0 - 1) && (ry < BY || gj == nn1 - 1) && (rz < BZ || gk == nn2 - 1);
+      if (f != nullptr && own) dot = fma(__ldg(f + g), v, dot);
+    }
+    sm[row * PITCH + q] = v;
+  }
+  __syncthreads();
+  const int tx = t % BX, ty = (t / BX) % BY, tz = t / (BX * BY);
+  const int ex = i0 + tx, ey = j0 + ty, ez = k0 + tz;
+  if (ex < ne0 && ey < ne1 && ez < ne2) {
+    double v[8][3];  // corner a = x + 2y + 4z
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double* S = sm + ((tz + (a >> 2)) * (BY + 1) + ty + ((a >> 1) & 1)) * PITCH + 3 * (tx + (a & 1));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[a][c] = S[c];
+    }
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1)  // in-place Walsh-Hadamard: v[s] = sum_a (-1)^{popcount(s & a)} v[a]
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (!(a & b))
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double x0 = v[a][c], x1 = v[a | b][c];
+            v[a][c] = x0 + x1;
+            v[a | b][c] = x0 - x1;
+          }
+    double s = 0.0;
+#pragma unroll
+    for (int chi = 0; chi < 8; ++chi)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int mi = f3h::blk_member(chi, i);
+        if (mi < 3) continue;  // the mean character: zero row
+        double y = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int mj = f3h::blk_member(chi, j);
+          if (f3h::blk_coef(chi, i, j) >= 0) y = fma(op.keh[f3h::blk_coef(chi, i, j)], v[mj / 3][mj % 3], y);
+        }
+        s = fma(v[mi / 3][mi % 3], y, s);
+      }
+    const long long e = ((long long)ez * ne1 + ey) * ne0 + ex;
+    if (ce) ce[e] = s;
+    if (dc) {
+      const double r = __ldg(rho + e);
+      dc[e] = -(p * (e0 - emin) * simp_pow_m1(r, p)) * s;
+    }
+  }
+  if (f) grid_reduce(dot, red);
+}
+
 // ----------------------------------------------------------------------------
 // ABI
 // ----------------------------------------------------------------------------
@@ -900,23 +989,36 @@ static dim3 sens3_grid(const Operator& o) {
   const unsigned want = std::max(1u, (4u * (unsigned)sms + gx * gy - 1) / (gx * gy));
   return dim3(gx, gy, std::min<unsigned>(want, (unsigned)std::max(1, o.ne[2])));
 }
-static bool sens_streamed(const Operator& o) {
-  static const bool on = [] {
-    const char* e = std::getenv("TMG_SENS_STREAM");
-    return e && e[0] == '1';  // 1: the z-streamed tile kernel k_sens3 (measured slower than the gather: A/B)
+// 3D sensitivity kernel (TMG_SENS=gather|stream|brick): 0 per-element gather (k_sens<3>, default: 65 us on
+// config 4), 1 z-streamed tiles (k_sens3: 87 us), 2 bricks staged in shared memory (k_sensb: 108 us) -- the two
+// staged forms read u once and coalesced but run at 2-3 CTAs per SM; the gather at full occupancy hides its
+// L1-served 8-fold node reuse better (profiles/r02_sens_ab.txt)
+static int sens_mode(const Operator& o) {
+  static const int mode = [] {
+    const char* e = std::getenv("TMG_SENS");
+    if (!e) return 0;
+    return e[0] == 'b' ? 2 : (e[0] == 's' ? 1 : 0);
   }();
-  return o.dim == 3 && on;
+  return o.dim == 3 ? mode : 0;
+}
+static bool sens_streamed(const Operator& o) { return sens_mode(o) == 1; }
+static dim3 sensb_grid(const Operator& o) {
+  return dim3((o.ne[0] + sensb::BX - 1) / sensb::BX, (o.ne[1] + sensb::BY - 1) / sensb::BY,
+              (o.ne[2] + sensb::BZ - 1) / sensb::BZ);
 }
 
 static void launch_sens(tmg_operator& K, const double* u, const double* f, double* ce, const double* rho, double p,
                         double e0, double emin, double* dc, cudaStream_t s) {
   const Operator& o = K.op;
-  const dim3 g3 = sens_streamed(o) ? sens3_grid(o) : dim3(1, 1, 1);
-  const unsigned g = sens_streamed(o) ? g3.x * g3.y * g3.z : sens_grid(o.nelem);
+  const int mode = sens_mode(o);
+  const dim3 g3 = mode == 1 ? sens3_grid(o) : (mode == 2 ? sensb_grid(o) : dim3(1, 1, 1));
+  const unsigned g = mode ? g3.x * g3.y * g3.z : sens_grid(o.nelem);
   if (f && K.sens.part.n < g) K.sens.alloc(g, s);
   const Red red = f ? K.sens.red() : Red{nullptr, nullptr, nullptr};
-  if (sens_streamed(o))
+  if (mode == 1)
     launch(k_sens3, g3, sens3::NT, 0, s, o.fine<3>(), u, f, ce, rho, p, e0, emin, dc, red);
+  else if (mode == 2)
+    launch(k_sensb, g3, sensb::NT, 0, s, o.fine<3>(), u, f, ce, rho, p, e0, emin, dc, red);
   else if (o.dim == 2)
     launch(k_sens<2>, g, TPB, 0, s, o.fine<2>(), u, f, o.nelem, o.ndof, ce, rho, p, e0, emin, dc, red);
   else
