@@ -210,6 +210,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+#ifndef TMG_F3H_POLL_NS
+#define TMG_F3H_POLL_NS 200
+#endif
 // (producer side: the slot frees up about once per layer -- back off between polls
 // instead of competing with the consumer warps for issue slots)
 __device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigned parity) {
@@ -223,7 +226,7 @@ __device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigne
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
     if (done) break;
-    __nanosleep(200);
+    __nanosleep(TMG_F3H_POLL_NS);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {

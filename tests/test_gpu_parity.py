@@ -280,3 +280,47 @@ def test_error_behaviour():
         T.SmootherConfig(weight=0.0)
     with pytest.raises(ValueError):
         T.cg_solve(K, np.zeros(3))
+
+
+_AB_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2001_01655_b200 as T
+from paper_2001_01655_b200 import problems
+w = problems.config_3(dims=(20, 10, 10))
+leg = w.solvers[0]
+K = T.assemble_stiffness(w.mesh, w.bc, w.moduli)
+h = T.build_gmg(w.mesh, K, 1, problems.gmg_settings(leg), leg["n_pre"], leg["n_post"], max_levels=3)
+u, rec = T.cg_solve(K, w.bc.load_vector, None, h, T.SolveConfig(method="cg", rtol=1e-8, max_iterations=25))
+b = np.random.default_rng(3).standard_normal(K.shape[0])
+z = h.apply(b)
+np.savez({out!r}, u=u.cpu().numpy(), z=z.cpu().numpy(), iterations=rec.iterations)
+"""
+
+
+@pytest.mark.parametrize("switch", ["TMG_CHEB_XONLY", "TMG_CHEB_RESIDUAL"])
+def test_chebyshev_shortcuts_do_not_change_the_vcycle(switch, tmp_path):
+    """The V-cycle's Chebyshev shortcuts are rearrangements of the reference's
+    order of work (multigrid.py:131-150, 231-244) that change the result by
+    fp64 rounding only: dropping the operator application of a pass's last step
+    when its residual is not read (TMG_CHEB_XONLY=0 restores it: the same
+    x += alpha (D^-1 r + beta p), up to the compiler's FMA contraction), and
+    reusing the maintained residual after pre-smoothing (TMG_CHEB_RESIDUAL=0
+    recomputes b - A x).  The switches are read once per process, so each
+    setting runs in its own interpreter."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for val in ("1", "0"):
+        env = dict(os.environ, **{switch: val})
+        out = str(tmp_path / ("ab_%s.npz" % val))
+        r = subprocess.run([sys.executable, "-c", _AB_SCRIPT.format(root=root, out=out)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(dict(np.load(out)))
+    assert int(outs[0]["iterations"]) == int(outs[1]["iterations"])
+    assert rel(outs[0]["z"], outs[1]["z"]) <= (1e-13 if switch == "TMG_CHEB_XONLY" else 1e-10)
+    assert rel(outs[0]["u"], outs[1]["u"]) <= 1e-8
