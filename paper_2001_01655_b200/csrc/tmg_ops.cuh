@@ -648,10 +648,85 @@ struct StencilOp {
   static constexpr int MINB = TMG_ST_MINB;  // large register budget: batched loads in flight
   static constexpr int THREADS = TPB;
   static constexpr bool STREAM = false;
+  // 3D symmetric storage (TMG_ST_SYM3): the centre block and, pair by pair, the
+  // upper block A_h(i) with x at node i + off and the transposed upper block of
+  // the node below, A_h(i - off)^T, with x at node i - off.  Every stored block is
+  // read by two rows (its owner's and the row of the node it couples to, one to
+  // nn0*nn1 nodes later): HBM sees 14 of the 27 blocks per node, the second
+  // read is an L2 hit.  GP pairs of loads (2 x 9 coefficients + 2 x 3 vector
+  // entries each) are in flight per batch.
+  template <class Src>
+  __device__ __forceinline__ void row_sym3(int node, int i, int j, int k, const Src& src, double out[3],
+                                           double self[3]) const {
+    const int n = (int)L.n;
+    double acc[3];
+    {
+      double xv[3], av[9];
+      src.load(node, i, j, k, xv);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) av[q] = ldv(A + q * n + node);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        self[a] = xv[a];
+        acc[a] = av[a * 3] * xv[0] + av[a * 3 + 1] * xv[1] + av[a * 3 + 2] * xv[2];
+      }
+    }
+    constexpr int GP = 2, NP = NS / 2;  // 13 pairs
+#pragma unroll
+    for (int h0 = 1; h0 <= NP; h0 += GP) {
+      double au[GP][9], al[GP][9], xu[GP][3], xl[GP][3];
+#pragma unroll
+      for (int g = 0; g < GP; ++g) {
+        const int h = h0 + g;
+        if (h > NP) {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) au[g][q] = al[g][q] = 0.0;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xu[g][d] = xl[g][d] = 0.0;
+          continue;
+        }
+        const int s = C0 + h, dx = Slots<3>::dx(s), dy = Slots<3>::dy(s), dz = Slots<3>::dz(s);
+        // upper neighbour (clamped: the stored block is zero when it is off the lattice)
+        const int iu = min(max(i + dx, 0), L.nn[0] - 1), ju = min(max(j + dy, 0), L.nn[1] - 1),
+                  ku = min(max(k + dz, 0), L.nn[2] - 1);
+        src.load(L.id(iu, ju, ku), iu, ju, ku, xu[g]);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) au[g][q] = ldv(A + (h * 9 + q) * n + node);
+        // lower neighbour: its upper block, transposed
+        const int il = i - dx, jl = j - dy, kl = k - dz;
+        const bool in = L.inside(il, jl, kl);
+        const int nb = in ? L.id(il, jl, kl) : node;
+        src.load(nb, in ? il : i, in ? jl : j, in ? kl : k, xl[g]);
+        if (!in) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xl[g][d] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) al[g][q] = ldv(A + (h * 9 + q) * n + nb);
+      }
+      reg_fence<GP * 9>(&au[0][0]);
+      reg_fence<GP * 9>(&al[0][0]);
+      reg_fence<GP * 3>(&xu[0][0]);
+      reg_fence<GP * 3>(&xl[0][0]);
+#pragma unroll
+      for (int g = 0; g < GP; ++g)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc[a] += au[g][a * 3 + b] * xu[g][b] + al[g][b * 3 + a] * xl[g][b];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c] = acc[c];
+  }
+
   template <class Src>
   __device__ void row(bool active, int node, int i, int j, int k, const Src& src, double out[DIM],
                       double self[DIM]) const {
     if (!active) return;
+    if constexpr (DIM == 3 && C0 > 0) {
+      row_sym3(node, i, j, k, src, out, self);
+      return;
+    }
     constexpr int G = DIM == 2 ? 9 : 3;
     double acc[DIM];
 #pragma unroll
