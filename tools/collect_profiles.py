@@ -96,7 +96,7 @@ def main():
             fh.write(ncu_summary.summary(launches, 60, 90) + "\n")
     summ_path = os.path.join(P, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    for name in ("cheb3d_bench", "cheb3d", "residual3d", "cheb3d_stencil", "cgpq3d", "sens", "dgemm", "dgemm_gram"):
+    for name in ("cheb3d_bench", "cheb3d", "residual3d", "cheb3d_stencil", "cgpq3d", "sens", "dgemm", "dgemm_gram", "gemv"):
         m = digest(name, r)
         if m and name == "cheb3d_bench":
             rd = to_bytes(*m["dram__bytes_read.sum"])

@@ -43,6 +43,7 @@ cap residual3d k_residualILi3ENS_6FineOp 1 4
 cap cheb3d_stencil k_chebILi3ENS_9StencilOp 1 4
 cap cgpq3d k_cg_pqILi3ENS_6FineOp 1 4
 cap dgemm_gram k_dgemm_tileILb1ELb0 0 1 gmg
+cap gemv k_gemv_split 2 1 gmg
 unset TMG_PCG_EAGER
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --kernel-name-base function -k regex:"k_dgemm_tile|k_chol|k_sym_from" \
   --log-file gpurun_out/launches_chol_$R.csv python tools/profile_case.py --config 1 --iters 2 --reps 1 --legs gmg > gpurun_out/ncu_chol.log 2>&1
