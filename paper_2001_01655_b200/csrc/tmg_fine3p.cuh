@@ -78,11 +78,24 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
       fin_m16[u] = (int)(((unsigned long long)op.mask + (unsigned long long)rowoff) & 15ull);
     }
   }
-  auto finish = [&](int r) {
-    const int p = z0 - 1 + r, s3 = r % NSR, su = r % NU;
-    mbar_wait(raw_full + s3, (unsigned)(r / NSR) & 1u);
+  // (the ring positions of the next plane to stage are carried from plane to plane:
+  // no division by the ring depths or multiplication by the plane size per step)
+  static_assert((NU & (NU - 1)) == 0, "finished-plane ring depth: a power of two");
+  int f_s3 = 0, f_su = 0, f_p = z0 - 1;
+  unsigned f_ph = 0u;
+  int f_pm16 = ((z0 - 1) * pl_m16) & 15;
+  auto finish = [&](int) {
+    const int p = f_p, s3 = f_s3, su = f_su;
+    mbar_wait(raw_full + s3, f_ph);
     const bool pin = p >= 0 && p < nn2;
-    const int ppar = p & pl_par, pm16 = (p * pl_m16) & 15;
+    const int ppar = p & pl_par, pm16 = f_pm16;
+    ++f_p;
+    f_pm16 = (f_pm16 + pl_m16) & 15;
+    f_su = (f_su + 1) & (NU - 1);
+    if (++f_s3 == NSR) {
+      f_s3 = 0;
+      f_ph ^= 1u;
+    }
 #pragma unroll
     for (int u = 0; u < NFIN; ++u) {
       if (u > 0 && fin_st[u] >= NS) break;
@@ -111,9 +124,11 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
   };
 
   // ---- A warps: epilogue inputs, output ----
+  long long node_k = own_node2d + plane * (z0 - 1);  // the own node in plane k (advanced with k)
+  const double* Ep = op.E + own_el2d + eplane * (z0 + 1);  // the own element in layer k + 2
   auto load_epi = [&](int pk, double (*e)[3]) {
     const bool ok = out_ok && pk >= z0 && pk < z1;
-    const long long node = own_node2d + plane * pk;
+    const long long node = node_k;  // (pk == k)
 #pragma unroll
     for (int v = 0; v < NVE; ++v)
 #pragma unroll
@@ -122,11 +137,14 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
   auto load_E = [&](int k) {
     return (el_ok && k >= 0 && k < ne2 && k < z1) ? __ldg(op.E + k * eplane + own_el2d) : 0.0;
   };
+  auto load_E2 = [&](int k2) {  // layer k2 = k + 2 through the running pointer
+    return (el_ok && k2 >= 0 && k2 < ne2 && k2 < z1) ? __ldg(Ep) : 0.0;
+  };
   double epre[NVE][3], W0[3] = {0.0, 0.0, 0.0};
   auto output = [&](int k) {
     const int pk = k - 1;
     if (!(pk >= z0 && pk < z1 && out_ok)) return;
-    const int su = (pk - z0 + 1) % NU;
+    const int su = (int)((unsigned)(pk - z0 + 1) & (unsigned)(NU - 1));
     const double* Xb = X + (pk & 1) * X_PLANE + t - TX;
     const double* Us = S + su * U_PLANE + own_st;
     const unsigned mk = M[su * NS + own_st];
@@ -137,7 +155,7 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
       const double acc = W0[c] + Xb[c * NC];
       out[c] = ((mk >> c) & 1u) ? acc : self[c];
     }
-    epi((int)(own_node2d + plane * pk), gi, gj, pk, out, self, epre);
+    epi((int)(node_k - plane), gi, gj, pk, out, self, epre);  // (pk == k - 1)
   };
 
   // ---- both halves: the owned characters of a face, a layer ----
@@ -160,7 +178,7 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
   // layer k: bottom characters Fb, top Ft (computed here); G: the bottom plane's
   // sums (completed here), T: the next plane's (produced here)
   auto layer = [&](int k, double Ek, const double (*Fb)[2], double (*Ft)[2], double (*G)[2], double (*T)[2]) {
-    face((k + 2 - z0) % NU, Ft);
+    face((int)((unsigned)(k + 2 - z0) & (unsigned)(NU - 1)), Ft);
     bool tset[3][2] = {};
 #pragma unroll
     for (int chi = 0; chi < 8; ++chi) {
@@ -245,11 +263,13 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
     if (H == 0) output(k);                                                     \
     const double Ek = Enext;                                                   \
     Enext = Enext2;                                                            \
-    Enext2 = load_E(k + 2);                                                    \
+    Enext2 = load_E2(k + 2);                                                   \
     if (H == 0) load_epi(k, epre);                                             \
     if (H == 1 && k + 3 - z0 <= R) finish(k + 3 - z0);                         \
     layer(k, Ek, Fb, Ft, Ga, Gb);                                              \
     ++k;                                                                       \
+    node_k += plane;                                                           \
+    Ep += eplane;                                                              \
   }
   for (; k + 1 < z1;) {
     TMG_F3P_STEP(F0, F1, G0, G1)
