@@ -128,11 +128,13 @@ __device__ __forceinline__ void fine3p_consumer(const FineOp<3>& op, const Src& 
   const double* Ep = op.E + own_el2d + eplane * (z0 + 1);  // the own element in layer k + 2
   auto load_epi = [&](int pk, double (*e)[3]) {
     const bool ok = out_ok && pk >= z0 && pk < z1;
-    const long long node = node_k;  // (pk == k)
+    const int node = (int)node_k;  // (pk == k; node ids fit an int, as in the epilogues)
 #pragma unroll
-    for (int v = 0; v < NVE; ++v)
+    for (int v = 0; v < NVE; ++v) {
+      const double* ev = ein.v[v] + 3ll * node;  // (32 x 32 -> 64-bit multiply-add: one instruction)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) e[v][c] = (ok && ein.v[v]) ? __ldg(ein.v[v] + 3 * node + c) : 0.0;
+      for (int c = 0; c < 3; ++c) e[v][c] = (ok && ein.v[v]) ? __ldg(ev + c) : 0.0;
+    }
   };
   auto load_E = [&](int k) {
     return (el_ok && k >= 0 && k < ne2 && k < z1) ? __ldg(op.E + k * eplane + own_el2d) : 0.0;
